@@ -1,0 +1,150 @@
+/* ww.h — C ABI of the B200-native fused ternary widely-linear GEMV
+ * (FairyFuse, arXiv 2604.20913).
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * Operation (Eq. 1; Eqs. 2-3; Alg. 1):
+ *   y = U x + W conj(x)                     (WW_CONV_EQ1, default)
+ *   y = (U + conj(W)) x   == Eqs. 2-3        (WW_CONV_ALG1)
+ *   U = diag(sUr) U_re + i diag(sUi) U_im,  W = diag(sWr) W_re + i diag(sWi) W_im,
+ *   U_re, U_im, W_re, W_im in {-1,0,+1}^{n x m}; the only multiplies are the 8 scale
+ *   multiplies per output row after accumulation.
+ *
+ * Ternary code (App. H): 2 bits (b1,b0), (1,0) = +1, (0,1) = -1,
+ * (0,0) = 0, (1,1) unused.  Layouts of the packed weights (all little-endian uint32):
+ *   WW_LAYOUT_PLANAR: the paper's App. H format.  Four planes back to back in the order
+ *     U_re, U_im, W_re, W_im; each plane row-major n x W words, W = ceil(m/16);
+ *     column j of a row is slot (j % 16) of word (j / 16): bit 2k+1 = +1, bit 2k = -1;
+ *     padding columns carry the zero code.
+ *   WW_LAYOUT_COL4 (device layout, consumed by the GPU kernels): row-major n x W "chunks"
+ *     of 16 bytes (one uint4 per 16 columns); byte k of chunk c of row i holds the four
+ *     codes of column 16c+k with the App. H bit rule applied per plane:
+ *     bit 2p+1 = (plane p code == +1), bit 2p = (plane p code == -1), p = 0..3 =
+ *     U_re, U_im, W_re, W_im.  Same 2 bits per code (n*W*16 bytes = n*m when 16 | m);
+ *     the bit order is chosen so one R2P decodes a column's predicates.
+ *
+ * Scales (R2): WW_SCALES_PER_ROW = n x 4 fp32 [sUr, sUi, sWr, sWi] row-major;
+ *   WW_SCALES_PER_TENSOR = 4 fp32 shared by all rows.
+ * Activations / outputs: complex64 = interleaved (re, im) fp32 pairs (torch.complex64).
+ *
+ * Conventions: every buffer is caller-allocated; the library never allocates or frees
+ * and holds no global state besides a thread-local error string.  Host functions are
+ * synchronous and thread-safe.  GPU entry points are asynchronous on `stream`
+ * (a cudaStream_t passed as void*, NULL = legacy default stream), never synchronize,
+ * validate arguments before launching, and map launch failures to WW_ERR_CUDA (faults
+ * inside a kernel surface at the caller's next synchronization).  Numerics: fp32
+ * round-to-nearest accumulation in an unspecified but deterministic order (bitwise
+ * repeatable for a given shape and batch), no FTZ, no fast-math.
+ */
+#ifndef WW_H
+#define WW_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WW_VERSION 1
+
+typedef enum {
+    WW_OK = 0,
+    WW_ERR_INVALID_ARGUMENT = 1,   /* null pointer, n<1, m<1, B<1, ld<m, world<1, rank out of range */
+    WW_ERR_DIMENSION_MISMATCH = 2, /* e.g. ldx < m, ldy < n */
+    WW_ERR_INVALID_CODE = 3,       /* dense weight value not in {-1,0,+1} */
+    WW_ERR_INVALID_ENCODING = 4,   /* slot pattern (1,1) met while unpacking */
+    WW_ERR_NONFINITE_SCALE = 5,    /* reserved: scales live on the device and are not inspected */
+    WW_ERR_MISALIGNED = 6,         /* packed not 16-B aligned, x / y not 8-B aligned */
+    WW_ERR_UNSUPPORTED = 7,        /* B > WW_MAX_BATCH, layout not COL4 on the GPU, ... */
+    WW_ERR_CUDA = 8                /* a CUDA runtime call failed; see ww_last_error() */
+} ww_status;
+
+typedef enum { WW_LAYOUT_PLANAR = 0, WW_LAYOUT_COL4 = 1 } ww_layout;
+typedef enum { WW_CONV_EQ1 = 0, WW_CONV_ALG1 = 1 } ww_convention;
+typedef enum { WW_SCALES_PER_TENSOR = 0, WW_SCALES_PER_ROW = 1 } ww_scale_mode;
+
+/* launch flags (ww_layer.flags) */
+#define WW_FLAG_PDL 1u /* programmatic dependent launch: the kernel starts streaming its
+                          weights while the previous kernel on the stream finishes, and
+                          waits (griddepcontrol.wait) before touching x, y or scales */
+
+#define WW_MAX_BATCH 16
+
+/* One widely-linear layer (complex n x m).  Fields are fixed-width for a stable ABI. */
+typedef struct {
+    int64_t n;          /* complex output rows, >= 1 */
+    int64_t m;          /* complex input columns, >= 1 */
+    int32_t layout;     /* ww_layout of the packed weights (GPU: WW_LAYOUT_COL4) */
+    int32_t scale_mode; /* ww_scale_mode */
+    int32_t conv;       /* ww_convention */
+    uint32_t flags;     /* WW_FLAG_* */
+} ww_layer;
+
+/* Bytes of packed weights for an n x m layer in either layout: 16 * n * ceil(m/16). */
+size_t ww_packed_bytes(int64_t n, int64_t m);
+
+/* Host packer (App. H).  u_re..w_im: dense int8 n x m planes, row stride ld
+ * (>= m) elements; values must be in {-1,0,+1} (else WW_ERR_INVALID_CODE, nothing
+ * promised about `out`).  out: ww_packed_bytes(n,m) bytes, caller-owned host memory. */
+ww_status ww_pack_ternary(const int8_t* u_re, const int8_t* u_im, const int8_t* w_re,
+                          const int8_t* w_im, int64_t n, int64_t m, int64_t ld, int32_t layout,
+                          uint32_t* out);
+
+/* Host unpacker (inverse).  Rejects slot (1,1) with WW_ERR_INVALID_ENCODING. */
+ww_status ww_unpack_ternary(const uint32_t* packed, int64_t n, int64_t m, int32_t layout,
+                            int8_t* u_re, int8_t* u_im, int8_t* w_re, int8_t* w_im, int64_t ld);
+
+/* Host re-layout between WW_LAYOUT_PLANAR and WW_LAYOUT_COL4 (src and dst distinct). */
+ww_status ww_repack(const uint32_t* src, int32_t src_layout, int64_t n, int64_t m,
+                    uint32_t* dst, int32_t dst_layout);
+
+/* Device packer: dense int8 planes on the GPU -> WW_LAYOUT_COL4 on the GPU.
+ * planes_d: 4 planes (U_re, U_im, W_re, W_im) of n x ld int8 back to back (plane p at
+ * planes_d + p*n*ld).  out_d: ww_packed_bytes(n,m) bytes, 16-B aligned.  bad_d (may be
+ * NULL): device int32 set to 1 if any value is outside {-1,0,+1} (that column then packs
+ * as zero); it is never cleared by the library.  Asynchronous on `stream`. */
+ww_status ww_pack_ternary_device(const int8_t* planes_d, int64_t n, int64_t m, int64_t ld,
+                                 uint32_t* out_d, int32_t* bad_d, void* stream);
+
+/* Fused WL-GEMV, one vector (B = 1).  packed_d: WW_LAYOUT_COL4, 16-B aligned;
+ * scales_d: per row n x 4 or per tensor 4 fp32; x_d: m complex64; y_d: n complex64
+ * (x and y must not alias).  Asynchronous on `stream`. */
+ww_status ww_wl_gemv(const ww_layer* L, const void* packed_d, const float* scales_d,
+                     const float* x_d, float* y_d, void* stream);
+
+/* Batched small-B variant, 1 <= B <= WW_MAX_BATCH: X_d is B rows of m complex64 with row
+ * stride ldx (complex elements, >= m); Y_d is B rows of n complex64 with stride ldy
+ * (>= n).  Every decoded code drives all B vectors (one pass over the weights). */
+ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d, const float* scales_d,
+                             const float* X_d, int64_t ldx, float* Y_d, int64_t ldy, int32_t B,
+                             void* stream);
+
+/* Row sharding over `world` GPUs (ceil blocks so an all-gather has equal counts):
+ * rows_per_rank = ceil(n/world), n_padded = world*rows_per_rank, rank r owns rows
+ * [r*rpr, min((r+1)*rpr, n)) (possibly empty).  Its COL4/PLANAR-row weights are the
+ * contiguous byte range [packed_offset_bytes, +packed_bytes) of a COL4 buffer, its
+ * per-row scales the floats [scale_offset_floats, +scale_count), and its outputs go to
+ * complex offset y_offset_complex of the gathered vector (B = 1; for B > 1 the gathered
+ * buffer is rank-major [world][B][rows_per_rank]). */
+typedef struct {
+    int32_t world, rank;
+    int64_t n, rows_per_rank, n_padded, row_begin, row_end;
+    int64_t packed_offset_bytes, packed_bytes, scale_offset_floats, scale_count,
+        y_offset_complex;
+} ww_shard;
+ww_status ww_shard_plan(int64_t n, int64_t m, int32_t world, int32_t rank, ww_shard* out);
+
+/* Launch configuration the GPU entry points use for (L, B): grid/block/dynamic smem,
+ * rows per CTA and x column-tile width (chunks).  Pure host function. */
+typedef struct {
+    int32_t grid, block, smem_bytes, tiles, tile_chunks, num_sms;
+} ww_launch_info;
+ww_status ww_query_launch(const ww_layer* L, int32_t B, ww_launch_info* out);
+
+const char* ww_status_string(ww_status s);
+const char* ww_last_error(void); /* thread-local message of the last failing call */
+int32_t ww_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,227 @@
+"""Python binding of ``libww.so`` — the C ABI in ``include/ww.h``.
+
+Argument marshalling only: every step of the WL-GEMV runs in the library's CUDA
+kernels (or its host packer).  PyTorch supplies device memory and streams.  If
+the in-tree ``libww.so`` is missing this module raises at import time: there is
+no CPU or PyTorch fallback for any entry point.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libww.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                      f"g.build()'` (no fallback path exists)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# --------------------------------------------------------------------------- enums
+OK = 0
+ERR_INVALID_ARGUMENT, ERR_DIMENSION_MISMATCH, ERR_INVALID_CODE, ERR_INVALID_ENCODING = 1, 2, 3, 4
+ERR_NONFINITE_SCALE, ERR_MISALIGNED, ERR_UNSUPPORTED, ERR_CUDA = 5, 6, 7, 8
+LAYOUT_PLANAR, LAYOUT_COL4 = 0, 1
+CONV_EQ1, CONV_ALG1 = 0, 1
+SCALES_PER_TENSOR, SCALES_PER_ROW = 0, 1
+FLAG_PDL = 1
+MAX_BATCH = 16
+
+# every symbol include/ww.h declares (tests check the library exports them all)
+EXPORTS = ("ww_packed_bytes", "ww_pack_ternary", "ww_unpack_ternary", "ww_repack",
+           "ww_pack_ternary_device", "ww_wl_gemv", "ww_wl_gemv_batched", "ww_shard_plan",
+           "ww_query_launch", "ww_status_string", "ww_last_error", "ww_version")
+
+
+class WWError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{status_string(status)}: {msg}")
+        self.status = status
+
+
+class _Layer(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("layout", ctypes.c_int32),
+                ("scale_mode", ctypes.c_int32), ("conv", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+class _Shard(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32)] + [
+        (f, ctypes.c_int64) for f in ("n", "rows_per_rank", "n_padded", "row_begin", "row_end",
+                                      "packed_offset_bytes", "packed_bytes",
+                                      "scale_offset_floats", "scale_count", "y_offset_complex")]
+
+
+class _LaunchInfo(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in ("grid", "block", "smem_bytes", "tiles",
+                                              "tile_chunks", "num_sms")]
+
+
+_i64, _i32, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+_lib.ww_packed_bytes.restype = ctypes.c_size_t
+_lib.ww_packed_bytes.argtypes = [_i64, _i64]
+_lib.ww_pack_ternary.restype = _i32
+_lib.ww_pack_ternary.argtypes = [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp]
+_lib.ww_unpack_ternary.restype = _i32
+_lib.ww_unpack_ternary.argtypes = [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _i64]
+_lib.ww_repack.restype = _i32
+_lib.ww_repack.argtypes = [_vp, _i32, _i64, _i64, _vp, _i32]
+_lib.ww_pack_ternary_device.restype = _i32
+_lib.ww_pack_ternary_device.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _vp]
+_lib.ww_wl_gemv.restype = _i32
+_lib.ww_wl_gemv.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _vp, _vp]
+_lib.ww_wl_gemv_batched.restype = _i32
+_lib.ww_wl_gemv_batched.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _i64, _vp, _i64, _i32,
+                                    _vp]
+_lib.ww_shard_plan.restype = _i32
+_lib.ww_shard_plan.argtypes = [_i64, _i64, _i32, _i32, ctypes.POINTER(_Shard)]
+_lib.ww_query_launch.restype = _i32
+_lib.ww_query_launch.argtypes = [ctypes.POINTER(_Layer), _i32, ctypes.POINTER(_LaunchInfo)]
+_lib.ww_status_string.restype = ctypes.c_char_p
+_lib.ww_status_string.argtypes = [_i32]
+_lib.ww_last_error.restype = ctypes.c_char_p
+_lib.ww_last_error.argtypes = []
+_lib.ww_version.restype = _i32
+_lib.ww_version.argtypes = []
+
+
+def status_string(s: int) -> str:
+    return _lib.ww_status_string(s).decode()
+
+
+def last_error() -> str:
+    return _lib.ww_last_error().decode()
+
+
+def version() -> int:
+    return int(_lib.ww_version())
+
+
+def _check(st: int):
+    if st != OK:
+        raise WWError(st, last_error())
+
+
+# --------------------------------------------------------------------------- layer
+@dataclass
+class Layer:
+    """A complex n x m widely-linear layer (ww_layer)."""
+    n: int
+    m: int
+    layout: int = LAYOUT_COL4
+    scale_mode: int = SCALES_PER_ROW
+    conv: int = CONV_EQ1
+    flags: int = 0
+
+    def c(self) -> _Layer:
+        return _Layer(self.n, self.m, self.layout, self.scale_mode, self.conv, self.flags)
+
+
+def packed_bytes(n: int, m: int) -> int:
+    return int(_lib.ww_packed_bytes(n, m))
+
+
+# --------------------------------------------------------------------------- host packer
+def pack_ternary(planes: np.ndarray, layout: int = LAYOUT_COL4) -> np.ndarray:
+    """(4, n, m) int8 planes U_re, U_im, W_re, W_im -> packed uint32 words (host)."""
+    p = np.ascontiguousarray(planes, dtype=np.int8)
+    _, n, m = p.shape
+    out = np.empty(packed_bytes(n, m) // 4, dtype=np.uint32)
+    _check(_lib.ww_pack_ternary(p[0].ctypes.data, p[1].ctypes.data, p[2].ctypes.data,
+                                p[3].ctypes.data, n, m, m, layout, out.ctypes.data))
+    return out
+
+
+def unpack_ternary(packed: np.ndarray, n: int, m: int, layout: int = LAYOUT_COL4) -> np.ndarray:
+    w = np.ascontiguousarray(packed, dtype=np.uint32)
+    assert w.nbytes == packed_bytes(n, m)
+    out = np.empty((4, n, m), dtype=np.int8)
+    _check(_lib.ww_unpack_ternary(w.ctypes.data, n, m, layout, out[0].ctypes.data,
+                                  out[1].ctypes.data, out[2].ctypes.data, out[3].ctypes.data, m))
+    return out
+
+
+def repack(packed: np.ndarray, n: int, m: int, src_layout: int, dst_layout: int) -> np.ndarray:
+    w = np.ascontiguousarray(packed, dtype=np.uint32)
+    out = np.empty_like(w)
+    _check(_lib.ww_repack(w.ctypes.data, src_layout, n, m, out.ctypes.data, dst_layout))
+    return out
+
+
+# --------------------------------------------------------------------------- device entry points
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def pack_ternary_device(planes, bad=None, stream=None, out=None):
+    """(4, n, ld) int8 CUDA tensor -> COL4 packed uint8 CUDA tensor of packed_bytes(n, m)."""
+    import torch
+    assert planes.is_cuda and planes.dtype == torch.int8 and planes.is_contiguous()
+    _, n, ld = planes.shape
+    m = ld
+    if out is None:
+        out = torch.empty(packed_bytes(n, m), dtype=torch.uint8, device=planes.device)
+    _check(_lib.ww_pack_ternary_device(planes.data_ptr(), n, m, ld, out.data_ptr(),
+                                       bad.data_ptr() if bad is not None else None,
+                                       _stream_ptr(stream)))
+    return out
+
+
+def wl_gemv(layer: Layer, packed, scales, x, y=None, stream=None):
+    """y = WL-GEMV(x) for one complex64 CUDA vector x of length m."""
+    import torch
+    if y is None:
+        y = torch.empty(layer.n, dtype=torch.complex64, device=x.device)
+    L = layer.c()
+    _check(_lib.ww_wl_gemv(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(), x.data_ptr(),
+                           y.data_ptr(), _stream_ptr(stream)))
+    return y
+
+
+def wl_gemv_batched(layer: Layer, packed, scales, X, Y=None, stream=None):
+    """Y[b] = WL-GEMV(X[b]) for a (B, m) complex64 CUDA tensor (row stride X.stride(0))."""
+    import torch
+    B = X.shape[0]
+    if Y is None:
+        Y = torch.empty((B, layer.n), dtype=torch.complex64, device=X.device)
+    L = layer.c()
+    _check(_lib.ww_wl_gemv_batched(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(),
+                                   X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0), B,
+                                   _stream_ptr(stream)))
+    return Y
+
+
+# --------------------------------------------------------------------------- sharding / launch
+@dataclass(frozen=True)
+class Shard:
+    world: int
+    rank: int
+    n: int
+    rows_per_rank: int
+    n_padded: int
+    row_begin: int
+    row_end: int
+    packed_offset_bytes: int
+    packed_bytes: int
+    scale_offset_floats: int
+    scale_count: int
+    y_offset_complex: int
+
+
+def shard_plan(n: int, m: int, world: int, rank: int) -> Shard:
+    s = _Shard()
+    _check(_lib.ww_shard_plan(n, m, world, rank, ctypes.byref(s)))
+    return Shard(*[getattr(s, f) for f, _ in _Shard._fields_])
+
+
+def query_launch(layer: Layer, B: int = 1) -> dict:
+    li = _LaunchInfo()
+    L = layer.c()
+    _check(_lib.ww_query_launch(ctypes.byref(L), B, ctypes.byref(li)))
+    return {f: getattr(li, f) for f, _ in _LaunchInfo._fields_}

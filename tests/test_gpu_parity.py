@@ -1,0 +1,201 @@
+"""GPU parity: the sm_100a WL-GEMV kernels (through the C ABI) against the C fp64
+oracle on the same seeded inputs.  Bar (R8): rel L2 <= 1e-5 and per element
+|err| <= 1e-4 * max_c s_c(i) * sum_j |x_j|.  Integer work (packing) is bit-exact."""
+import numpy as np
+import pytest
+
+import oracle as orc
+import ww_inputs as wi
+from _wl import LayerCase, assert_parity
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - GPU box only
+    pytest.skip("no CUDA device", allow_module_level=True)
+import paper_2604_20913_b200 as ww  # noqa: E402
+
+CONVS = [ww.CONV_EQ1, ww.CONV_ALG1]
+ORC = {ww.CONV_EQ1: orc.CONV_EQ1, ww.CONV_ALG1: orc.CONV_ALG1}
+
+
+@pytest.mark.parametrize("spec", [wi.C1, wi.C2, wi.C3A, wi.C3B], ids=lambda s: s.name)
+@pytest.mark.parametrize("conv", CONVS)
+def test_baseline_configs_full(spec, conv):
+    case = LayerCase.from_spec(spec, seed=0).device(ww, torch)
+    y = case.gpu(ww, torch, conv)
+    assert_parity(y, case.oracle(ORC[conv]), case)
+
+
+@pytest.mark.parametrize("B", wi.C5_BATCHES)
+@pytest.mark.parametrize("conv", CONVS)
+def test_config5_batched_full(B, conv):
+    case = LayerCase.from_spec(wi.C3B, seed=5, B=B).device(ww, torch)
+    y = case.gpu(ww, torch, conv)
+    assert_parity(y, case.oracle(ORC[conv]), case)
+
+
+SHAPES = [(1, 1), (1, 15), (15, 1), (16, 16), (17, 17), (63, 64), (64, 65), (65, 63),
+          (128, 1000), (1000, 128), (149, 17), (300, 513), (2, 4097)]
+
+
+@pytest.mark.parametrize("n,m", SHAPES)
+@pytest.mark.parametrize("conv", CONVS)
+@pytest.mark.parametrize("per_row", [True, False])
+def test_small_and_ragged_shapes(n, m, conv, per_row):
+    case = LayerCase(n, m, seed=n * 7919 + m, dist=wi.UNIFORM3, per_row=per_row,
+                     lo=0.5, hi=2.0).device(ww, torch)
+    assert_parity(case.gpu(ww, torch, conv), case.oracle(ORC[conv]), case)
+
+
+@pytest.mark.parametrize("B", list(range(1, 17)))
+def test_every_batch_size_and_batch_invariance(B):
+    n, m = 150, 333
+    case = LayerCase(n, m, seed=B, B=B).device(ww, torch)
+    yb = case.gpu(ww, torch, ww.CONV_EQ1)
+    assert_parity(yb, case.oracle(orc.CONV_EQ1), case)
+    # a vector's accumulation order does not depend on the rest of the batch: B <= 2 share
+    # the 2-set interleaved accumulators of B = 1, B >= 3 the single set
+    L = case.layer(ww, ww.CONV_EQ1)
+    for b in (0, B - 1):
+        if B <= 2:
+            y1 = ww.wl_gemv(L, case.packed_d, case.scales_d, case.x_d[b].contiguous())[None]
+        else:
+            X3 = torch.stack([case.x_d[b], case.x_d[0], case.x_d[B - 1]])
+            y1 = ww.wl_gemv_batched(L, case.packed_d, case.scales_d, X3)
+        assert np.array_equal(y1[0].cpu().numpy(), yb[b])
+
+
+def test_multi_tile_long_rows():
+    # x larger than one shared-memory tile (B=1: 96 KB = 12288 complex columns)
+    case = LayerCase(40, 20000, seed=3).device(ww, torch)
+    assert ww.query_launch(case.layer(ww, 0), 1)["tiles"] > 1
+    for conv in CONVS:
+        assert_parity(case.gpu(ww, torch, conv), case.oracle(ORC[conv]), case)
+
+
+def test_batched_multi_tile_and_waves():
+    # B=16 on 2048 x 5504 uses column tiles; 5000 rows forces several row waves per CTA
+    case = LayerCase(5000, 1111, seed=4, B=16).device(ww, torch)
+    assert ww.query_launch(case.layer(ww, 0), 16)["tiles"] > 1
+    assert_parity(case.gpu(ww, torch, ww.CONV_ALG1), case.oracle(orc.CONV_ALG1), case)
+
+
+def test_zero_and_identity_exact():
+    n = m = 257
+    x = wi.activations(9, m)
+    planes = np.zeros((4, n, m), np.int8)
+    case = LayerCase(n, m, planes=planes, scales=np.ones((n, 4), np.float32), x=x).device(ww, torch)
+    assert not case.gpu(ww, torch, ww.CONV_EQ1).any()
+    planes[0] = np.eye(n, dtype=np.int8)
+    case = LayerCase(n, m, planes=planes, scales=np.ones(4, np.float32), x=x).device(ww, torch)
+    for conv in CONVS:
+        assert np.array_equal(case.gpu(ww, torch, conv)[0], x[0])
+
+
+def test_conventions_differ_only_in_w_terms():
+    case = LayerCase(64, 96, seed=12).device(ww, torch)
+    a = case.gpu(ww, torch, ww.CONV_EQ1)
+    b = case.gpu(ww, torch, ww.CONV_ALG1)
+    assert np.array_equal(a.real, b.real)  # y_re is the same expression (Eq. 2)
+    assert not np.array_equal(a.imag, b.imag)
+
+
+def test_determinism_and_pdl_flag():
+    case = LayerCase.from_spec(wi.C2, seed=1).device(ww, torch)
+    ys = [case.gpu(ww, torch, ww.CONV_EQ1) for _ in range(3)]
+    ys.append(case.gpu(ww, torch, ww.CONV_EQ1, flags=ww.FLAG_PDL))
+    for y in ys[1:]:
+        assert np.array_equal(y, ys[0])
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_shard_invariance_emulated(world):
+    # each rank's slice run on its own (n_local rows), concatenated == unsharded, bitwise
+    spec = wi.C3A
+    case = LayerCase.from_spec(spec, seed=2).device(ww, torch)
+    full = case.gpu(ww, torch, ww.CONV_EQ1)[0]
+    gathered = torch.zeros(ww.shard_plan(spec.n, spec.m, world, 0).n_padded, dtype=torch.complex64,
+                           device="cuda")
+    for r in range(world):
+        s = ww.shard_plan(spec.n, spec.m, world, r)
+        if s.row_end == s.row_begin:
+            continue
+        L = ww.Layer(s.row_end - s.row_begin, spec.m)
+        pk = case.packed_d[s.packed_offset_bytes:s.packed_offset_bytes + s.packed_bytes]
+        sc = case.scales_d.reshape(-1)[s.scale_offset_floats:s.scale_offset_floats + s.scale_count]
+        out = gathered[s.y_offset_complex:s.y_offset_complex + (s.row_end - s.row_begin)]
+        ww.wl_gemv(L, pk, sc, case.x_d[0], out)
+    torch.cuda.synchronize()
+    assert np.array_equal(gathered[:spec.n].cpu().numpy(), full)
+
+
+def test_slot_11_contributes_add_then_subtract():
+    # (1,1) is never packed; the kernel applies Eq. 6 then Eq. 7 (x - x), a zero contribution
+    # up to rounding (R3): parity with the oracle treating those codes as 0.
+    n, m = 33, 64
+    case = LayerCase(n, m, seed=21).device(ww, torch)
+    ref = case.oracle(orc.CONV_EQ1)
+    words = ww.pack_ternary(case.planes, ww.LAYOUT_COL4).copy()
+    zero_cols = np.argwhere(case.planes[1] == 0)[:50]
+    for i, j in zero_cols:  # U_im code (plane 1) of column j: bits 2, 3 of byte j%16
+        w = (i * ((m + 15) // 16) + j // 16) * 4 + (j % 16) // 4
+        words[w] |= 0x3 << (8 * (j % 4) + 2)
+    case.packed_d = torch.from_numpy(words.view(np.uint8)).cuda()
+    assert_parity(case.gpu(ww, torch, ww.CONV_EQ1), ref, case)
+
+
+def test_unaligned_x_path():
+    # x at an 8-byte (not 16-byte) offset exercises the 8-byte cp.async staging path
+    case = LayerCase(100, 77, seed=8).device(ww, torch)
+    buf = torch.zeros(78, dtype=torch.complex64, device="cuda")
+    buf[1:] = case.x_d[0]
+    y = ww.wl_gemv(case.layer(ww, ww.CONV_EQ1), case.packed_d, case.scales_d, buf[1:])
+    torch.cuda.synchronize()
+    assert_parity(y.cpu().numpy()[None], case.oracle(orc.CONV_EQ1), case)
+
+
+def test_device_packer_bit_exact():
+    n, m = 333, 1000
+    planes = wi.planes(17, n, m)
+    d = torch.from_numpy(planes).cuda().contiguous()
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    got = ww.pack_ternary_device(d, bad)
+    torch.cuda.synchronize()
+    want = ww.pack_ternary(planes, ww.LAYOUT_COL4).view(np.uint8)
+    assert np.array_equal(got.cpu().numpy(), want) and int(bad.item()) == 0
+    d[2, 5, 7] = 3
+    ww.pack_ternary_device(d, bad)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 1
+
+
+def test_device_generated_codes_pack_like_host():
+    n, m = 512, 2048
+    d = torch.empty((4, n, m), dtype=torch.int8, device="cuda")
+    for p in range(4):
+        wi.codes_device(77, p, n, m, d[p])
+    got = ww.pack_ternary_device(d)
+    torch.cuda.synchronize()
+    want = ww.pack_ternary(wi.planes(77, n, m), ww.LAYOUT_COL4).view(np.uint8)
+    assert np.array_equal(got.cpu().numpy(), want)
+
+
+def test_argument_errors_before_launch():
+    case = LayerCase(8, 32, seed=1).device(ww, torch)
+    L = case.layer(ww, ww.CONV_EQ1)
+    y = torch.empty(8, dtype=torch.complex64, device="cuda")
+    with pytest.raises(ww.WWError) as e:
+        ww.wl_gemv(L, case.packed_d[1:], case.scales_d, case.x_d[0], y)
+    assert e.value.status == ww.ERR_MISALIGNED
+    X = torch.zeros((17, 32), dtype=torch.complex64, device="cuda")
+    with pytest.raises(ww.WWError) as e:
+        ww.wl_gemv_batched(L, case.packed_d, case.scales_d, X)
+    assert e.value.status == ww.ERR_UNSUPPORTED
+    with pytest.raises(ww.WWError) as e:
+        ww.wl_gemv(ww.Layer(8, 32, layout=ww.LAYOUT_PLANAR), case.packed_d, case.scales_d,
+                   case.x_d[0], y)
+    assert e.value.status == ww.ERR_UNSUPPORTED
+    with pytest.raises(ww.WWError) as e:
+        ww.wl_gemv(L, case.packed_d, case.scales_d, case.x_d[0], case.x_d[0].view(torch.complex64))
+    assert e.value.status == ww.ERR_INVALID_ARGUMENT
