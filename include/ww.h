@@ -133,8 +133,10 @@ typedef struct {
 } ww_shard;
 ww_status ww_shard_plan(int64_t n, int64_t m, int32_t world, int32_t rank, ww_shard* out);
 
-/* Launch configuration the GPU entry points use for (L, B): grid/block/dynamic smem,
- * rows per CTA and x column-tile width (chunks).  Pure host function. */
+/* Launch configuration the GPU entry points use for (L, B): grid (one CTA per SM, each
+ * owning a contiguous row range), block, dynamic shared memory, the number of x column
+ * tiles and their width (16-column chunks), and the SM count it was planned for.
+ * Pure host function. */
 typedef struct {
     int32_t grid, block, smem_bytes, tiles, tile_chunks, num_sms;
 } ww_launch_info;

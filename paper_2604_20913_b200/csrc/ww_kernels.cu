@@ -28,8 +28,7 @@ namespace {
 // warps per CTA: 16 while the B accumulators leave room, 8 (255-register cap) above
 template <int B>
 __host__ __device__ constexpr int warps_for() { return B <= 4 ? 16 : 8; }
-constexpr int kMaxWarps = 16;
-constexpr int kXBudgetBytes = 96 * 1024;  // x tile per CTA (2 CTAs/SM fit for PDL overlap)
+constexpr int kXBudgetBytes = 184 * 1024;  // x tile per CTA (one CTA per SM)
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
@@ -69,22 +68,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 }
 
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
-
-// Eq. 6 then Eq. 7 for one code of one plane: bit (2p+1) adds X, bit 2p subtracts X.
-#define WW_PLANE(ACC, BITS, P, X, NX)                   \
-    do {                                                \
-        if ((BITS) & (2u << (2 * (P)))) ACC = fadd2(ACC, X);  \
-        if ((BITS) & (1u << (2 * (P)))) ACC = fadd2(ACC, NX); \
-    } while (0)
-
-// One column (8 code bits = 4 planes) against one activation pair.
-__device__ __forceinline__ void column(float2 (&acc)[4], uint32_t bits, float2 x) {
-    const float2 nx = make_float2(-x.x, -x.y);
-    WW_PLANE(acc[0], bits, 0, x, nx);
-    WW_PLANE(acc[1], bits, 1, x, nx);
-    WW_PLANE(acc[2], bits, 2, x, nx);
-    WW_PLANE(acc[3], bits, 3, x, nx);
-}
 
 struct Params {
     const uint4* packed;  // COL4 chunks, row-major n x W
@@ -128,48 +111,85 @@ template <int B>
 __device__ __forceinline__ void stage_x(const Params& p, uint32_t xs, int64_t c0, int tc_lo,
                                         int tc_hi) {
     const int TC = p.tile_chunks;
-    const int span = tc_hi - tc_lo;
-    const int total = B * span * 8;
-    for (int g = threadIdx.x; g < total; g += blockDim.x) {
-        const int b = g / (span * 8);
-        const int rem = g - b * span * 8;
-        const int tc = tc_lo + (rem >> 3), gg = rem & 7;
-        const int64_t col = (c0 + tc) * 16 + 2 * gg;
-        const int64_t valid = p.m - col;  // columns left in this row of x
-        const float* src = p.X + 2 * (b * p.ldx + col);
-        const uint32_t dst = xs + (uint32_t)(((b * TC + tc) * 8 + (gg ^ (tc & 7))) * 16);
-        if (p.aligned16) {
-            const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
-            cp_async16(dst, bytes ? (const void*)src : (const void*)p.X, bytes);
-        } else {
-            cp_async8(dst, valid >= 1 ? (const void*)src : (const void*)p.X, valid >= 1 ? 8 : 0);
-            cp_async8(dst + 8, valid >= 2 ? (const void*)(src + 2) : (const void*)p.X,
-                      valid >= 2 ? 8 : 0);
+    const int span8 = (tc_hi - tc_lo) * 8;
+#pragma unroll 1
+    for (int b = 0; b < B; ++b) {
+        const float* xb = p.X + 2 * (b * p.ldx + (c0 + tc_lo) * 16);
+        const int64_t left0 = p.m - (c0 + tc_lo) * 16;  // valid columns from the slice start
+        const uint32_t base = xs + (uint32_t)((b * TC + tc_lo) * 128);
+        for (int g = threadIdx.x; g < span8; g += blockDim.x) {
+            const int tcl = g >> 3, gg = g & 7;  // tile chunk (relative), granule
+            const int64_t valid = left0 - 2 * g;   // columns left at this granule
+            const float* src = xb + 4 * g;
+            const uint32_t dst = base + (uint32_t)((tcl * 8 + (gg ^ ((tc_lo + tcl) & 7))) * 16);
+            if (p.aligned16) {
+                const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
+                cp_async16(dst, bytes ? (const void*)src : (const void*)p.X, bytes);
+            } else {
+                cp_async8(dst, valid >= 1 ? (const void*)src : (const void*)p.X, valid >= 1 ? 8 : 0);
+                cp_async8(dst + 8, valid >= 2 ? (const void*)(src + 2) : (const void*)p.X,
+                          valid >= 2 ? 8 : 0);
+            }
         }
     }
 }
 
-// Accumulators: S interleaved sets (ILP + shorter fp32 chains) of B x 4 pair accumulators.
+// Accumulators: S column-parity sets of B x 4 pair sums.  For B <= 2 even and odd columns
+// feed separate sets (more independent FADD2 chains per warp, half-length fp32 chains);
+// larger B has ILP across vectors.  N = 2 would keep separate positive / negative sums
+// (acc = pos - neg); measured no faster on B200, so N = 1.
 template <int B>
 struct Acc {
-    static constexpr int S = B <= 2 ? 2 : 1;
-    float2 a[S][B][4];
+    static constexpr int S = B <= 2 ? 2 : 1;  // column-parity sets
+    static constexpr int N = 1;
+    float2 a[S][N][B][4];
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
-            for (int b = 0; b < B; ++b)
+            for (int k = 0; k < N; ++k)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) a[s][b][q] = make_float2(0.f, 0.f);
+                for (int b = 0; b < B; ++b)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) a[s][k][b][q] = make_float2(0.f, 0.f);
+    }
+    // sum over sets of plane q, vector b: pos - neg
+    __device__ __forceinline__ float2 total(int b, int q) const {
+        float2 t = a[0][0][b][q];
+        if (S == 2) t = fadd2(t, a[S - 1][0][b][q]);
+        if (N == 2) {
+            float2 n = a[0][N - 1][b][q];
+            if (S == 2) n = fadd2(n, a[S - 1][N - 1][b][q]);
+            t = fadd2(t, make_float2(-n.x, -n.y));
+        }
+        return t;
     }
 };
 
-// One 16-column chunk of one row (its 16-byte COL4 word w) against the staged x of tile
-// chunk tc: 64 codes x B vectors, 2 predicated FADD2 per code and vector.
+// One column (8 code bits = 4 planes) against one activation pair: Eq. 6 (bit 2p+1, add)
+// and Eq. 7 (bit 2p, subtract) for each plane p.
+template <int N>
+__device__ __forceinline__ void column(float2 (&pos)[4], float2 (&neg)[4], uint32_t bits, float2 x) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (bits & (2u << (2 * q))) pos[q] = fadd2(pos[q], x);
+        if (N == 2) {
+            if (bits & (1u << (2 * q))) neg[q] = fadd2(neg[q], x);
+        } else {
+            if (bits & (1u << (2 * q))) pos[q] = fadd2(pos[q], make_float2(-x.x, -x.y));
+        }
+    }
+}
+
+// One 16-column chunk of one row (its 16-byte COL4 word w) against the staged x of that
+// chunk: 64 codes x B vectors, 2 predicated FADD2 per code and vector.  xc = smem address of
+// the chunk's x for vector 0 (vector b at xc + b*bstride); off[kk] = swizzled offset of
+// column pair kk ((kk ^ (lane & 7)) * 16: the chunk index's low bits are the lane's).
 template <int B>
-__device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xs, int TC, int tc) {
+__device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xc, uint32_t bstride,
+                                      const uint32_t (&off)[8]) {
+    constexpr int S = Acc<B>::S, N = Acc<B>::N;
     const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
-    const uint32_t sw = (uint32_t)(tc & 7);
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {  // column pair (2kk, 2kk+1)
         const uint32_t word = w4[kk >> 1];
@@ -177,9 +197,9 @@ __device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xs, i
         const uint32_t bits_a = (word >> sh) & 0xffu, bits_b = (word >> (sh + 8)) & 0xffu;
 #pragma unroll
         for (int b = 0; b < B; ++b) {  // each decoded code drives all B vectors (a9)
-            const float4 v = lds128(xs + (uint32_t)((((b * TC + tc) * 8) + (kk ^ sw)) * 16));
-            column(acc.a[0][b], bits_a, make_float2(v.x, v.y));
-            column(acc.a[Acc<B>::S - 1][b], bits_b, make_float2(v.z, v.w));
+            const float4 v = lds128(xc + b * bstride + off[kk]);
+            column<N>(acc.a[0][0][b], acc.a[0][N - 1][b], bits_a, make_float2(v.x, v.y));
+            column<N>(acc.a[S - 1][0][b], acc.a[S - 1][N - 1][b], bits_b, make_float2(v.z, v.w));
         }
     }
 }
@@ -208,10 +228,11 @@ __device__ __forceinline__ void warp_transpose_reduce(float (&v)[NV]) {
     }
 }
 
-// Row finished: reduce the 8B sums over the warp, apply the 8 scales once per row and vector
-// (P:1002-1011), write y.  sc = this warp's scratch (next_pow2(8B) floats).
+// Warp reduction of this warp's 8B partial sums (a7): writes the NV = next_pow2(8B) totals
+// [A0.re A0.im A1.re A1.im A2.re A2.im A3.re A3.im] x B to smem `dst` (only the lanes that
+// hold them write).  Ends with __syncwarp.
 template <int B>
-__device__ __forceinline__ void finish_row(const Params& p, Acc<B>& acc, int64_t row, float* sc) {
+__device__ __forceinline__ void reduce_to(const Acc<B>& acc, float* dst) {
     const int lane = threadIdx.x & 31;
     constexpr int NV = next_pow2(8 * B);
     float v[NV];
@@ -219,8 +240,7 @@ __device__ __forceinline__ void finish_row(const Params& p, Acc<B>& acc, int64_t
     for (int b = 0; b < B; ++b)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            float2 t = acc.a[0][b][q];
-            if (Acc<B>::S == 2) t = fadd2(t, acc.a[Acc<B>::S - 1][b][q]);
+            const float2 t = acc.total(b, q);
             v[8 * b + 2 * q] = t.x;
             v[8 * b + 2 * q + 1] = t.y;
         }
@@ -234,15 +254,21 @@ __device__ __forceinline__ void finish_row(const Params& p, Acc<B>& acc, int64_t
     for (int r = 0; r < H; ++r) idx = (idx << 1) | ((lane >> (4 - r)) & 1);
     if ((lane & ((1 << (5 - H)) - 1)) == 0) {
 #pragma unroll
-        for (int s = 0; s < C; ++s) sc[idx * C + s] = v[s];
+        for (int s = 0; s < C; ++s) dst[idx * C + s] = v[s];
     }
     __syncwarp();
+}
+
+// Epilogue (a8): lane b < B applies the row's 8 scales once to the totals T
+// of vector b and stores y.
+template <int B>
+__device__ __forceinline__ void epilogue(const Params& p, const float* T0, int64_t row) {
+    const int lane = threadIdx.x & 31;
     if (lane < B) {
-        const float* T = sc + 8 * lane;
+        const float* T = T0 + 8 * lane;
         const float* s = p.scales + (p.per_row_scales ? 4 * row : 0);
         const float sUr = s[0], sUi = s[1], sWr = s[2], sWi = s[3];
-        // T = [A0.re A0.im A1.re A1.im A2.re A2.im A3.re A3.im], A_p = sum_j t_pj (x_re,j, x_im,j)
-        const float yre = sUr * T[0] - sUi * T[3] + sWr * T[4] + sWi * T[7];
+        const float yre = sUr * T[0] - sUi * T[3] + sWr * T[4] + sWi * T[7];          // Eq. 2
         const float yim = p.conv == WW_CONV_EQ1
                               ? sUr * T[1] + sUi * T[2] - sWr * T[5] + sWi * T[6]   // Eq. 1
                               : sUr * T[1] + sUi * T[2] + sWr * T[5] - sWi * T[6];  // Eq. 3
@@ -251,24 +277,44 @@ __device__ __forceinline__ void finish_row(const Params& p, Acc<B>& acc, int64_t
     __syncwarp();
 }
 
+// Shared-memory carve-up (bytes), identical on host (plan) and device.
+struct SmemLayout {
+    int64_t x_bytes, scratch_off, bar_off, total;
+};
+__host__ __device__ inline SmemLayout smem_layout(int B, int TC, int warps, int ntiles) {
+    const int64_t nv = next_pow2(8 * B);
+    SmemLayout L;
+    L.x_bytes = (int64_t)B * TC * 128;
+    L.scratch_off = L.x_bytes;
+    L.bar_off = L.scratch_off + (int64_t)warps * nv * 4;
+    const int64_t nbars = ntiles == 1 ? (TC + 31) / 32 : 0;
+    L.total = L.bar_off + 8 * nbars;
+    return L;
+}
+
+// register cap: B == 1 keeps <= 64 registers so two CTAs fit an SM and a PDL-launched next
+// layer can start on every SM while this one drains
 template <int B>
-__global__ void __launch_bounds__(warps_for<B>() * 32, B == 1 ? 2 : 1)
+__host__ __device__ constexpr int min_blocks() { return B == 1 ? 2 : 1; }
+
+template <int B>
+__global__ void __launch_bounds__(warps_for<B>() * 32, min_blocks<B>())
 wl_gemv_kernel(const Params p) {
-    constexpr int kWarps = warps_for<B>();
     constexpr int NV = next_pow2(8 * B);
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t xs = (uint32_t)__cvta_generic_to_shared(smem);
     const int TC = p.tile_chunks;
-    float* scratch = reinterpret_cast<float*>(smem + (size_t)B * TC * 128);
-    const uint32_t bars = xs + (uint32_t)(B * TC * 128 + kMaxWarps * NV * 4);
+    const int nwarps = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* sc = scratch + warp * NV;
     const int J = (TC + 31) / 32;  // lane sweeps per tile
+    const SmemLayout SL = smem_layout(B, TC, nwarps, p.ntiles);
+    float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * NV;
+    const uint32_t bars = xs + (uint32_t)SL.bar_off;
 
-    // balanced contiguous row range of this CTA (A12 row-parallel decomposition)
+    // balanced contiguous row range of this CTA (A12 row-parallel decomposition);
+    // the host sizes the CTA so its rows split into equal waves over its warps
     const int64_t r0 = (int64_t)blockIdx.x * p.n / gridDim.x;
     const int64_t r1 = (int64_t)(blockIdx.x + 1) * p.n / gridDim.x;
-
     const bool single = p.ntiles == 1;
     if (single && threadIdx.x == 0)
         for (int j = 0; j < J; ++j) mbar_init(bars + 8 * j, blockDim.x);
@@ -285,55 +331,60 @@ wl_gemv_kernel(const Params p) {
     Acc<B> acc;
     acc.zero();
 
+    uint32_t off[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) off[kk] = (uint32_t)((kk ^ (lane & 7)) << 4);
+    const uint32_t bstride = (uint32_t)TC * 128u;
+
     if (single) {
-        // flattened (row, sweep) items of this warp; weights prefetched 3 items ahead in
-        // registers, across row boundaries
-        const int64_t myrows = r0 + warp < r1 ? (r1 - r0 - warp + kWarps - 1) / kWarps : 0;
-        const int64_t total = myrows * J;
-        int64_t pf_row = r0 + warp;
+        // This warp's rows r0 + warp + k*nwarps, each swept in J steps of 32 chunks (lane =
+        // chunk within the step; the last step has `lastw` active lanes).  The weights stream
+        // two steps ahead in registers across row boundaries; all loop state is incremental.
+        const int lastw = TC - 32 * (J - 1);
+        const int64_t myrows = r0 + warp < r1 ? (r1 - r0 - warp + nwarps - 1) / nwarps : 0;
+        const uint4* pf = p.packed + (r0 + warp) * p.W + lane;  // prefetch pointer
+        const int64_t row_jump = (int64_t)nwarps * p.W - 32 * J;
+        int64_t pf_rows = myrows;
         int pf_j = 0;
         auto load_next = [&]() -> uint4 {
             uint4 w = make_uint4(0, 0, 0, 0);
-            const int tc = lane + 32 * pf_j;
-            if (pf_row < r1 && tc < TC) w = ldg_stream(p.packed + pf_row * p.W + tc);
+            if (pf_rows > 0 && (pf_j < J - 1 || lane < lastw)) w = ldg_stream(pf);
+            pf += 32;
             if (++pf_j == J) {
                 pf_j = 0;
-                pf_row += kWarps;
+                pf += row_jump;
+                --pf_rows;
             }
             return w;
         };
-        uint4 q0 = load_next(), q1 = load_next(), q2 = load_next();
+        uint4 qa = load_next(), qb = load_next();
         __syncthreads();  // mbarrier inits visible
         pdl_wait();
         for (int j = 0; j < J; ++j) {  // x in 32-chunk slices, each completing its mbarrier
             stage_x<B>(p, xs, 0, 32 * j, 32 * j + 32 < TC ? 32 * j + 32 : TC);
             cp_async_arrive(bars + 8 * j);
         }
+        const uint32_t xlane = xs + (uint32_t)lane * 128u;
         int64_t row = r0 + warp;
-        int j = 0;
-        bool first = true;
-        for (int64_t it = 0; it < total; ++it) {
-            const uint4 cur = q0;
-            q0 = q1;
-            q1 = q2;
-            q2 = load_next();
-            if (first) mbar_wait0(bars + 8 * j);
-            const int tc = lane + 32 * j;
-            if (tc < TC) chunk<B>(acc, cur, xs, TC, tc);
-            if (++j == J) {
-                finish_row<B>(p, acc, row, sc);
-                acc.zero();
-                j = 0;
-                first = false;
-                row += kWarps;
+        for (int64_t k = 0; k < myrows; ++k, row += nwarps) {
+            uint32_t xc = xlane;
+            for (int j = 0; j < J; ++j, xc += 4096u) {
+                const uint4 cur = qa;
+                qa = qb;
+                qb = load_next();
+                if (k == 0) mbar_wait0(bars + 8 * j);
+                if (j < J - 1 || lane < lastw) chunk<B>(acc, cur, xc, bstride, off);
             }
+            reduce_to<B>(acc, sc);
+            epilogue<B>(p, sc, row);
+            acc.zero();
         }
         return;
     }
 
     // x does not fit one tile: row waves, each streaming the tiles with CTA-wide syncs
     pdl_wait();
-    for (int64_t wr = r0; wr < r1; wr += kWarps) {  // uniform across the CTA
+    for (int64_t wr = r0; wr < r1; wr += nwarps) {  // uniform across the CTA
         const int64_t row = wr + warp;
         const bool active = row < r1;
         for (int t = 0; t < p.ntiles; ++t) {
@@ -350,13 +401,14 @@ wl_gemv_kernel(const Params p) {
                 for (; tc < tc_n; tc += 32) {
                     const uint4 nxt =
                         tc + 32 < tc_n ? ldg_stream(wrow + tc + 32) : make_uint4(0, 0, 0, 0);
-                    chunk<B>(acc, cur, xs, TC, tc);
+                    chunk<B>(acc, cur, xs + (uint32_t)tc * 128u, bstride, off);
                     cur = nxt;
                 }
             }
         }
         if (active) {
-            finish_row<B>(p, acc, row, sc);
+            reduce_to<B>(acc, sc);
+            epilogue<B>(p, sc, row);
             acc.zero();
         }
     }
@@ -418,14 +470,18 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
         tc = std::max<int64_t>(32, tc / 32 * 32);  // whole lane sweeps per tile
     }
     const int64_t ntiles = (W + tc - 1) / tc;
+    // one CTA per SM (persistent); a CTA's rows split into equal waves over its warps
     const int64_t grid = std::min<int64_t>(sms, L->n);
+    const int max_warps = B <= 4 ? 16 : 8;
+    const int64_t rows_cta = (L->n + grid - 1) / grid;
+    const int64_t waves = (rows_cta + max_warps - 1) / max_warps;
+    const int warps = (int)((rows_cta + waves - 1) / waves);
+    const SmemLayout SL = smem_layout(B, (int)tc, warps, (int)ntiles);
     li->grid = (int32_t)grid;
-    li->block = 32 * (B <= 4 ? 16 : 8);
+    li->block = 32 * warps;
     li->tile_chunks = (int32_t)tc;
     li->tiles = (int32_t)ntiles;
-    const int64_t nvp = next_pow2(8 * B);
-    const int64_t nbars = ntiles == 1 ? (tc + 31) / 32 : 0;
-    li->smem_bytes = (int32_t)(per_chunk * tc + (int64_t)kMaxWarps * nvp * 4 + 8 * nbars);
+    li->smem_bytes = (int32_t)SL.total;
     li->num_sms = sms;
     return WW_OK;
 }
@@ -436,7 +492,7 @@ cudaError_t launch_b(const Params& p, const ww_launch_info& li, cudaStream_t s, 
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(wl_gemv_kernel<B>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kXBudgetBytes + kMaxWarps * 128 * 4 + 8 * 64);
+                                             227 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -530,6 +586,7 @@ extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
     p.conv = L->conv;
     p.tile_chunks = li.tile_chunks;
     p.ntiles = li.tiles;
+
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
     cudaError_t e = launch(p, li, B, (cudaStream_t)stream, (L->flags & WW_FLAG_PDL) != 0);
     if (e != cudaSuccess)
