@@ -1,0 +1,491 @@
+"""Benchmark of the fused ternary widely-linear GEMV (FairyFuse, arXiv 2604.20913) on B200.
+
+Default workload (BASELINE.json config 4, the 7B decode linear stack): one step = one token
+through 32 decoder layers x 7 widely-linear projections (q,k,v,o 2048->2048; gate,up
+2048->5504; down 5504->2048, complex), B = 1, every projection's output rows sharded over
+the GPUs and all-gathered (NCCL).  The 1.62 GB of packed weights per step is > 12x L2, so
+every step streams its weights from HBM (no flush needed).
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload c4|c2|c3a|c3b|c5] [--batch B]
+    python bench.py --impl reference ...    # the C fp64 oracle on the host cores
+
+Prints ONE JSON line on rank 0 (contract in the task statement; fields documented in
+DESIGN.md §8).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "WL-GEMV packed-weight HBM GB/s (% of B200 peak), us/layer at 7B shapes"
+L2_BYTES = 126 * 2**20
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id, self.rows, self.proc, self.thread = gpu_id, [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self, peaks):
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else peaks.get("sm_max_mhz"),
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- distributed
+def _dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def _gpu_id(local):
+    import torch
+    try:
+        u = str(torch.cuda.get_device_properties(local).uuid)
+        return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        return vis.split(",")[local] if vis else str(local)
+
+
+# --------------------------------------------------------------------------- oracle (CPU)
+def oracle_sample(layers=(0,), seed=0, rows=None):
+    """Generate (host, untimed) the planar inputs of the listed decoder layers' 7 projections."""
+    import oracle as orc
+    import ww_inputs as wi
+    work = []
+    for l in layers:
+        for p, spec in enumerate(wi.C4_PROJS):
+            s = wi.layer_seed(seed, l, p)
+            nr = spec.n if rows is None else min(rows, spec.n)
+            planes = wi.planes(s, spec.n, spec.m, spec.dist, 0, nr)
+            sc = wi.scales(s, spec.n, True, spec.scale_lo, spec.scale_hi)[:nr]
+            x = wi.activations(s, spec.m, 1)
+            work.append((orc.pack_planar(planes), nr, spec.m, np.ascontiguousarray(sc), x))
+    return work
+
+
+def oracle_time(work):
+    import oracle as orc
+    t = time.perf_counter()
+    nbytes = 0
+    for planar, nr, m, sc, x in work:
+        orc.wl_direct(planar, nr, m, sc, x, orc.CONV_EQ1)
+        nbytes += 16 * nr * ((m + 15) // 16)
+    return time.perf_counter() - t, nbytes
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the C fp64 oracle as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    work = oracle_sample(layers=(0,), seed=args.seed)
+    for _ in range(args.warmup):
+        oracle_time(work)
+    ts, nb = [], 0
+    for _ in range(args.steps):
+        dt, nb = oracle_time(work)
+        ts.append(dt)
+    t = float(np.sum(ts))
+    value = nb * args.steps / t / 1e9
+    sample = ("decoder layer 0 of config 4 (q,k,v,o 2048x2048; gate,up 5504x2048; down "
+              "2048x5504), all rows, B=1, EQ1, orc_wl_direct (unpack to dense fp64 complex + "
+              "direct evaluation) per step")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c4_llama2_7b_wl_decode_stack (oracle sample)", "batch": 1,
+                   "sample": sample},
+        "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_20913_b200 as ww
+    from paper_2604_20913_b200.stack import WLStack
+    import ww_inputs as wi
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    peaks, peak_kind = _peaks()
+    group = dist.group.WORLD if world > 1 else None
+
+    if args.workload == "c4":
+        stack = WLStack(layers=args.layers, seed=args.seed, B=args.batch, rank=rank, world=world,
+                        pdl=not args.no_pdl, device=dev, group=group)
+        units = [stack]
+        layers_per_step = len(stack.projs)
+        workload = f"c4_llama2_7b_wl_decode_stack ({args.layers} layers x 7 projections)"
+    else:
+        # single-layer configs: R replicas of the layer (>= 4x L2) cycled inside a step
+        spec = {"c2": wi.C2, "c3a": wi.C3A, "c3b": wi.C3B, "c5": wi.C3B, "c1": wi.C1}[args.workload]
+        stack = _ReplicaLayer(spec, args, rank, world, dev, group)
+        units = [stack]
+        layers_per_step = stack.R
+        workload = f"{spec.name} x {stack.R} rotating replicas (>= 4x L2)"
+
+    s = torch.cuda.Stream(dev)
+    launches_per_step = 0
+    with torch.cuda.stream(s):
+        for _ in range(max(args.warmup, 3)):
+            launches_per_step = stack.step(s)
+    torch.cuda.synchronize(dev)
+
+    graph = None
+    if not args.no_graph:
+        try:
+            with torch.cuda.stream(s):
+                stack.step(s)  # one more eager step right before capture
+            torch.cuda.synchronize(dev)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                stack.step(s)
+            with torch.cuda.stream(s):
+                for _ in range(2):
+                    graph.replay()
+            torch.cuda.synchronize(dev)
+        except Exception as e:  # NCCL capture unsupported -> eager steps
+            graph = None
+            if rank == 0:
+                print(f"# graph capture failed ({e!r}); timing eager steps", file=sys.stderr)
+            torch.cuda.synchronize(dev)
+
+    def one_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            stack.step(s)
+
+    # ---------------- timed region: device time, barrier + sync on both sides, max over ranks
+    clocks = ClockSampler(_gpu_id(local))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    time.sleep(0.15)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(args.steps):
+            one_step()
+        e1.record(s)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+
+    # whole-job algorithmic bytes per step (sum over ranks)
+    alg = torch.tensor([stack.algorithmic_bytes(), stack.packed_act_bytes(), stack.adds()],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(alg)
+    alg_bytes, pa_bytes, adds = (float(v) for v in alg.tolist())
+    value = alg_bytes / (ms_step * 1e-3) / 1e9
+
+    # ---------------- per-shape kernel time: a CUDA graph of the same projection of every
+    # layer (distinct weights, so HBM-cold), CUDA events on the launching stream
+    per_shape = {}
+    kern_ms_total = 0.0
+    if args.workload == "c4":
+        for p_idx, key in ((0, "q/k/v/o"), (4, "gate/up"), (6, "down")):
+            idx = [i for i, pr in enumerate(stack.projs) if pr.proj == p_idx]
+            pr0 = stack.projs[idx[0]]
+            label = f"{key} {pr0.ylocal}x{pr0.spec.m}"
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(s):
+                    for i in idx:
+                        stack.launch(i, s)
+                torch.cuda.synchronize(dev)
+                with torch.cuda.graph(g, stream=s):
+                    for i in idx:
+                        stack.launch(i, s)
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(s):
+                    g.replay()
+                    a.record(s)
+                    for _ in range(5):
+                        g.replay()
+                    b.record(s)
+                torch.cuda.synchronize(dev)
+                per_shape[label] = round(a.elapsed_time(b) * 1e3 / (5 * len(idx)), 3)
+                kern_ms_total += per_shape[label] * 1e-3 * sum(
+                    1 for pr in stack.projs if pr.proj in
+                    ({0: (0, 1, 2, 3), 4: (4, 5), 6: (6,)}[p_idx]))
+            except Exception as e:  # pragma: no cover
+                per_shape[label] = f"unavailable: {e!r}"
+
+    # ---------------- e2e: host activations in, result out, through the same API calls
+    e2e = _e2e(stack, args, s, dev, graph, world, alg_bytes)
+
+    # ---------------- roofline of the dominant kernel (wl_gemv_kernel: every launch)
+    # at N=1 the timed step is nothing but WL-GEMV launches, so the kernel's average launch
+    # duration is step time / launches; at N>1 the eager per-launch events are used
+    launches = max(launches_per_step, 1)
+    if world == 1:
+        kern_ms_step = ms_step
+    else:
+        kern_ms_step = kern_ms_total if kern_ms_total > 0 else ms_step
+    per_launch_s = kern_ms_step * 1e-3 / launches
+    clk = clocks.summary(peaks)
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = 128 * nsm * sm_mhz * 1e6 / 1e12  # fp32 add lanes x SMs x max clock, T add/s
+    rank_adds = stack.adds()
+    achieved_alu = rank_adds / launches / per_launch_s / 1e12
+    rank_pa = stack.packed_act_bytes()
+    hbm_achieved = rank_pa / launches / per_launch_s / 1e9
+    roof = {"bound": "alu", "achieved": round(achieved_alu, 4), "peak": round(alu_peak, 4),
+            "unit": "Tadd/s", "frac": round(achieved_alu / alu_peak, 4),
+            "traffic": _ncu_traffic(),
+            "kernel": "wl_gemv_kernel<1>",
+            "peak_basis": f"128 fp32 add lanes/clk/SM x {nsm} SMs x {sm_mhz:.0f} MHz (DESIGN.md §8)",
+            "hbm": {"achieved": round(hbm_achieved, 1), "peak": peaks.get("hbm_gbs"),
+                    "unit": "GB/s", "frac": round(hbm_achieved / peaks.get("hbm_gbs", 6650.0), 4),
+                    "peak_kind": peak_kind, "bytes": "packed weights + x per launch"}}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        work = oracle_sample(layers=(0,), seed=args.seed)
+        dt, nb = oracle_time(work)
+        cpu = {"value": round(nb / dt / 1e9, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": "decoder layer 0 of config 4 (7 projections, all rows, B=1, EQ1), "
+                         f"{nb} packed bytes in {dt:.2f} s, single-threaded C fp64 oracle"}
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "strong" if args.workload == "c4" else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload, "batch": args.batch, "layers_per_step": layers_per_step,
+                   "parallelism": f"rows/{world} + NCCL all-gather" if world > 1 else "1 GPU",
+                   "graph": graph is not None, "pdl": not args.no_pdl,
+                   "l2": "inputs > L2: 1.62 GB of weights per step streamed from HBM"
+                         if args.workload == "c4" else "rotating replicas >= 4x L2",
+                   "launch": ww.query_launch(ww.Layer(2048, 5504), args.batch)},
+        "us_per_layer": round(1e3 * ms_step / layers_per_step, 3),
+        "per_shape_us": per_shape,
+        "pct_of_hbm_peak": round(100 * (pa_bytes / (ms_step * 1e-3) / 1e9) / world
+                                 / peaks.get("hbm_gbs", 6650.0), 2),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def _ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def _e2e(stack, args, s, dev, graph, world, alg_bytes):
+    """Same metric with host<->device copies in the timed region: pinned host activations
+    -> HBM each step, the last projection's gathered output -> host each step."""
+    import torch
+    import torch.distributed as dist
+    xflat = stack.X.view(-1)
+    xh = torch.empty(xflat.numel(), dtype=torch.complex64).pin_memory()
+    xh.copy_(xflat.cpu())
+    last = stack.Y[-1]
+    yh = torch.empty(last.numel(), dtype=torch.complex64).pin_memory()
+    steps = max(2, args.steps)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(steps):
+            xflat.copy_(xh, non_blocking=True)
+            if graph is not None:
+                graph.replay()
+            else:
+                stack.step(s)
+            yh.copy_(last, non_blocking=True)
+        e1.record(s)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": round(alg_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8),
+            "ms_per_step": round(ms, 4)}
+
+
+class _ReplicaLayer:
+    """A single BASELINE layer shape with R rotating weight replicas (>= 4x L2 in total),
+    one step = one launch per replica; row-sharded like the stack when world > 1."""
+
+    def __init__(self, spec, args, rank, world, dev, group):
+        import torch
+        import paper_2604_20913_b200 as ww
+        import ww_inputs as wi
+        self.ww, self.spec, self.rank, self.world, self.group = ww, spec, rank, world, group
+        self.B = args.batch
+        sh = ww.shard_plan(spec.n, spec.m, world, rank)
+        self.shard, self.nloc = sh, sh.row_end - sh.row_begin
+        nb = self.nloc * ww.packed_bytes(1, spec.m)
+        self.R = max(1, int(np.ceil(4 * L2_BYTES / max(nb, 1))))
+        planes = torch.empty((4, max(self.nloc, 1), spec.m), dtype=torch.int8, device=dev)
+        for q in range(4):
+            wi.codes_device(args.seed, q, self.nloc, spec.m, planes[q], spec.dist, row0=sh.row_begin)
+        base = ww.pack_ternary_device(planes)
+        self.Wr = torch.empty((self.R, nb), dtype=torch.uint8, device=dev)
+        self.Wr[:] = base
+        sc = wi.scales(args.seed, spec.n, spec.per_row, spec.scale_lo, spec.scale_hi)
+        if spec.per_row:
+            sc = sc[sh.row_begin:sh.row_end]
+        self.S = torch.from_numpy(np.ascontiguousarray(sc)).to(dev)
+        self.X = torch.from_numpy(wi.activations(args.seed, spec.m, self.B)).to(dev)
+        self.Y = [torch.zeros(sh.n_padded * self.B, dtype=torch.complex64, device=dev)]
+        self.L = ww.Layer(self.nloc, spec.m, ww.LAYOUT_COL4,
+                          ww.SCALES_PER_ROW if spec.per_row else ww.SCALES_PER_TENSOR,
+                          ww.CONV_EQ1, 0 if args.no_pdl else ww.FLAG_PDL)
+
+    def step(self, s):
+        rpr = self.shard.rows_per_rank
+        yv = self.Y[0][self.rank * self.B * rpr:(self.rank + 1) * self.B * rpr].view(self.B, rpr)
+        for r in range(self.R):
+            self.ww.wl_gemv_batched(self.L, self.Wr[r], self.S, self.X, yv, stream=s)
+            if self.world > 1:
+                import torch.distributed as dist
+                n = self.Y[0].numel() // self.world
+                dist.all_gather_into_tensor(self.Y[0], self.Y[0][self.rank * n:(self.rank + 1) * n],
+                                            group=self.group)
+        return self.R
+
+    def algorithmic_bytes(self):
+        m, n, B = self.spec.m, self.nloc, self.B
+        return self.R * (n * self.ww.packed_bytes(1, m) + 8 * m * B + 8 * n * B + 16 * n)
+
+    def packed_act_bytes(self):
+        return self.R * (self.nloc * self.ww.packed_bytes(1, self.spec.m) + 8 * self.spec.m * self.B)
+
+    def adds(self):
+        return self.R * 8 * self.nloc * self.spec.m * self.B
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=("c4", "c1", "c2", "c3a", "c3b", "c5"), default="c4")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # contract: W >= 3
+    if args.impl == "reference":
+        # the oracle runs on rank 0's host cores; other ranks exit 0 without work
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
+    world, rank, local = _dist_init(args)
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -15,10 +15,13 @@
 //   * reduce (a7): warp transpose-reduce of the 8B partial sums, then
 //   * epilogue (a8; P:1002-1011 / P:1435): 8 scale multiplies per row and vector, EQ1 or
 //     ALG1 signs, one complex64 store.
+#include <cuda.h>  // CUtensorMap (types only; the encoder comes from the runtime entry point)
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 
 #include "ww.h"
 #include "ww_internal.h"
@@ -69,19 +72,54 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
-struct Params {
+#ifdef WW_TRACE
+// per-warp event timestamps (globaltimer ns) for tools/trace_kernel.py; not in the product build
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ void trace(int ev) {
+    if (g_trace && (threadIdx.x & 31) == 0 && ev < 32) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[((size_t)blockIdx.x * 32 + (threadIdx.x >> 5)) * 32 + ev] = t;
+    }
+}
+#else
+__device__ __forceinline__ void trace(int) {}
+#endif
+
+struct alignas(64) Params {
+    CUtensorMap tmap;     // x as a [B][W][32 floats] tensor, 128B-swizzled boxes (use_tma)
     const uint4* packed;  // COL4 chunks, row-major n x W
     const float* scales;  // n x 4 or 4
     const float* X;       // B x ldx complex64
     float* Y;             // B x ldy complex64
     int64_t n, m, W, ldx, ldy;
     int32_t per_row_scales, conv, tile_chunks, ntiles, aligned16;
+    int32_t x_stride;     // chunks per vector in the shared x tile (multiple of 32)
+    int32_t use_tma;      // stage x with cp.async.bulk.tensor (else per-thread cp.async)
 };
 
 __host__ __device__ constexpr int next_pow2(int v) {
     int p = 1;
     while (p < v) p <<= 1;
     return p;
+}
+
+// TMA (cp.async.bulk.tensor) load of one 32-chunk x box into shared memory, completing
+// `bytes` of transaction on mbarrier `bar`
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
 // mbarrier helpers (one barrier per 32-chunk x slice; completes once per launch, phase 0)
@@ -110,13 +148,13 @@ __device__ __forceinline__ void mbar_wait0(uint32_t bar) {
 template <int B>
 __device__ __forceinline__ void stage_x(const Params& p, uint32_t xs, int64_t c0, int tc_lo,
                                         int tc_hi) {
-    const int TC = p.tile_chunks;
+    const int XS = p.x_stride;
     const int span8 = (tc_hi - tc_lo) * 8;
 #pragma unroll 1
     for (int b = 0; b < B; ++b) {
         const float* xb = p.X + 2 * (b * p.ldx + (c0 + tc_lo) * 16);
         const int64_t left0 = p.m - (c0 + tc_lo) * 16;  // valid columns from the slice start
-        const uint32_t base = xs + (uint32_t)((b * TC + tc_lo) * 128);
+        const uint32_t base = xs + (uint32_t)((b * XS + tc_lo) * 128);
         for (int g = threadIdx.x; g < span8; g += blockDim.x) {
             const int tcl = g >> 3, gg = g & 7;  // tile chunk (relative), granule
             const int64_t valid = left0 - 2 * g;   // columns left at this granule
@@ -131,6 +169,42 @@ __device__ __forceinline__ void stage_x(const Params& p, uint32_t xs, int64_t c0
                           valid >= 2 ? 8 : 0);
             }
         }
+    }
+}
+
+// Single-tile staging of all of x, sliced for early start: granules (16 B = 2 columns) are
+// numbered g = (b*TC + tc)*8 + gg; slice j = 32-chunk sweep j of every vector completes
+// mbarrier j.  Each thread issues its granules in slice order and arrives on barrier j once
+// all of its slice-<=j copies are issued (cp.async.mbarrier.arrive fires when they land).
+template <int B>
+__device__ __forceinline__ void stage_x_sliced(const Params& p, uint32_t xs, uint32_t bars,
+                                               int J) {
+    const int TC = p.tile_chunks, XS = p.x_stride;
+    const int per_b = TC * 8;  // granules per vector
+    int next = 0;              // next slice barrier to arrive on
+    // iterate slice-major so a thread's copies are issued in slice order
+    for (int j = 0; j < J; ++j) {
+        const int g_lo = 256 * j, g_hi = (256 * j + 256 < per_b ? 256 * j + 256 : per_b);
+        const int span = g_hi - g_lo;
+        for (int t = threadIdx.x; t < B * span; t += blockDim.x) {
+            const int b = B == 1 ? 0 : t / span;
+            const int g = g_lo + (B == 1 ? t : t - b * span);
+            const int tc = g >> 3, gg = g & 7;
+            const int64_t col = (int64_t)tc * 16 + 2 * gg;
+            const int64_t valid = p.m - col;
+            const float* src = p.X + 2 * (b * p.ldx + col);
+            const uint32_t dst = xs + (uint32_t)(((b * XS + tc) * 8 + (gg ^ (tc & 7))) * 16);
+            if (p.aligned16) {
+                const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
+                cp_async16(dst, bytes ? (const void*)src : (const void*)p.X, bytes);
+            } else {
+                cp_async8(dst, valid >= 1 ? (const void*)src : (const void*)p.X, valid >= 1 ? 8 : 0);
+                cp_async8(dst + 8, valid >= 2 ? (const void*)(src + 2) : (const void*)p.X,
+                          valid >= 2 ? 8 : 0);
+            }
+        }
+        cp_async_arrive(bars + 8 * next);
+        ++next;
     }
 }
 
@@ -170,13 +244,16 @@ struct Acc {
 // and Eq. 7 (bit 2p, subtract) for each plane p.
 template <int N>
 __device__ __forceinline__ void column(float2 (&pos)[4], float2 (&neg)[4], uint32_t bits, float2 x) {
+    const float2 nx = make_float2(-x.x, -x.y);
+    // bits in ascending order (bit 2q = -1 of plane q, bit 2q+1 = +1) so the compiler can
+    // turn a column's 8 predicates into one R2P of bits 0..6 plus one bit test
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        if (bits & (2u << (2 * q))) pos[q] = fadd2(pos[q], x);
-        if (N == 2) {
-            if (bits & (1u << (2 * q))) neg[q] = fadd2(neg[q], x);
-        } else {
-            if (bits & (1u << (2 * q))) pos[q] = fadd2(pos[q], make_float2(-x.x, -x.y));
+    for (int k = 0; k < 8; ++k) {
+        const int q = k >> 1;
+        if (bits & (1u << k)) {
+            if (k & 1) pos[q] = fadd2(pos[q], x);
+            else if (N == 2) neg[q] = fadd2(neg[q], x);
+            else pos[q] = fadd2(pos[q], nx);
         }
     }
 }
@@ -281,14 +358,16 @@ __device__ __forceinline__ void epilogue(const Params& p, const float* T0, int64
 struct SmemLayout {
     int64_t x_bytes, scratch_off, bar_off, total;
 };
-__host__ __device__ inline SmemLayout smem_layout(int B, int TC, int warps, int ntiles) {
+// x tile first (1024-B aligned for the 128B-swizzled TMA boxes), then the per-warp reduction
+// scratch, then one mbarrier per 32-chunk x slice (single-tile launches)
+__host__ __device__ inline SmemLayout smem_layout(int B, int XS, int warps, int ntiles) {
     const int64_t nv = next_pow2(8 * B);
     SmemLayout L;
-    L.x_bytes = (int64_t)B * TC * 128;
+    L.x_bytes = (int64_t)B * XS * 128;
     L.scratch_off = L.x_bytes;
     L.bar_off = L.scratch_off + (int64_t)warps * nv * 4;
-    const int64_t nbars = ntiles == 1 ? (TC + 31) / 32 : 0;
-    L.total = L.bar_off + 8 * nbars;
+    const int64_t nbars = ntiles == 1 ? XS / 32 : 0;
+    L.total = L.bar_off + 8 * nbars + 1024;  // + alignment slack of the dynamic smem base
     return L;
 }
 
@@ -299,15 +378,17 @@ __host__ __device__ constexpr int min_blocks() { return B == 1 ? 2 : 1; }
 
 template <int B>
 __global__ void __launch_bounds__(warps_for<B>() * 32, min_blocks<B>())
-wl_gemv_kernel(const Params p) {
+wl_gemv_kernel(const __grid_constant__ Params p) {
     constexpr int NV = next_pow2(8 * B);
-    extern __shared__ __align__(128) unsigned char smem[];
-    const uint32_t xs = (uint32_t)__cvta_generic_to_shared(smem);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t xs = (raw + 1023u) & ~1023u;  // 1024-B aligned x tile
+    unsigned char* smem = smem_raw + (xs - raw);
     const int TC = p.tile_chunks;
     const int nwarps = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int J = (TC + 31) / 32;  // lane sweeps per tile
-    const SmemLayout SL = smem_layout(B, TC, nwarps, p.ntiles);
+    const SmemLayout SL = smem_layout(B, p.x_stride, nwarps, p.ntiles);
     float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * NV;
     const uint32_t bars = xs + (uint32_t)SL.bar_off;
 
@@ -316,11 +397,14 @@ wl_gemv_kernel(const Params p) {
     const int64_t r0 = (int64_t)blockIdx.x * p.n / gridDim.x;
     const int64_t r1 = (int64_t)(blockIdx.x + 1) * p.n / gridDim.x;
     const bool single = p.ntiles == 1;
-    if (single && threadIdx.x == 0)
-        for (int j = 0; j < J; ++j) mbar_init(bars + 8 * j, blockDim.x);
+    if (single && threadIdx.x == 0) {
+        for (int j = 0; j < J; ++j) mbar_init(bars + 8 * j, p.use_tma ? 1u : blockDim.x);
+        fence_barrier_init();
+    }
 
     // PDL: let the next kernel launch now and warm L2 with this CTA's weights (never written
     // by other kernels) before waiting for the producer of x / consumer of y.
+    trace(0);
     pdl_launch_dependents();
     if (threadIdx.x == 0) {
         const char* wb = reinterpret_cast<const char*>(p.packed + r0 * p.W);
@@ -334,7 +418,7 @@ wl_gemv_kernel(const Params p) {
     uint32_t off[8];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) off[kk] = (uint32_t)((kk ^ (lane & 7)) << 4);
-    const uint32_t bstride = (uint32_t)TC * 128u;
+    const uint32_t bstride = (uint32_t)p.x_stride * 128u;
 
     if (single) {
         // This warp's rows r0 + warp + k*nwarps, each swept in J steps of 32 chunks (lane =
@@ -359,25 +443,54 @@ wl_gemv_kernel(const Params p) {
         };
         uint4 qa = load_next(), qb = load_next();
         __syncthreads();  // mbarrier inits visible
+        trace(1);
         pdl_wait();
-        for (int j = 0; j < J; ++j) {  // x in 32-chunk slices, each completing its mbarrier
-            stage_x<B>(p, xs, 0, 32 * j, 32 * j + 32 < TC ? 32 * j + 32 : TC);
-            cp_async_arrive(bars + 8 * j);
-        }
-        const uint32_t xlane = xs + (uint32_t)lane * 128u;
-        int64_t row = r0 + warp;
-        for (int64_t k = 0; k < myrows; ++k, row += nwarps) {
-            uint32_t xc = xlane;
-            for (int j = 0; j < J; ++j, xc += 4096u) {
-                const uint4 cur = qa;
-                qa = qb;
-                qb = load_next();
-                if (k == 0) mbar_wait0(bars + 8 * j);
-                if (j < J - 1 || lane < lastw) chunk<B>(acc, cur, xc, bstride, off);
+        trace(2);
+        if (p.use_tma) {  // one thread: a 4 KB 128B-swizzled box per slice and vector
+            if (threadIdx.x == 0) {
+                for (int j = 0; j < J; ++j) {
+                    mbar_expect_tx(bars + 8 * j, (uint32_t)(B * 4096));
+#pragma unroll 1
+                    for (int b = 0; b < B; ++b)
+                        tma_load_3d(xs + (uint32_t)((b * p.x_stride + 32 * j) * 128), &p.tmap, 0,
+                                    32 * j, b, bars + 8 * j);
+                }
             }
-            reduce_to<B>(acc, sc);
-            epilogue<B>(p, sc, row);
-            acc.zero();
+        } else {
+            stage_x_sliced<B>(p, xs, bars, J);
+        }
+        trace(3);
+        int tr_sweep = 4;
+        const uint32_t xlane = xs + (uint32_t)lane * 128u;
+        const int64_t total = myrows * J;  // sweeps of this warp
+        int64_t row = r0 + warp;
+        int j = 0;
+        uint32_t xc = xlane;
+        bool first = true;  // x slices still to be waited for (first row only)
+        auto consume = [&](const uint4& w) {
+            if (first) mbar_wait0(bars + 8 * j);
+            trace(tr_sweep++);
+            if (j < J - 1 || lane < lastw) chunk<B>(acc, w, xc, bstride, off);
+            xc += 4096u;
+            if (++j == J) {
+                reduce_to<B>(acc, sc);
+                epilogue<B>(p, sc, row);
+                trace(tr_sweep++);
+                acc.zero();
+                j = 0;
+                xc = xlane;
+                row += nwarps;
+                first = false;
+            }
+        };
+        // unrolled by two with fixed registers: q0 holds even sweeps, q1 odd sweeps
+        for (int64_t s = 0; s < total; s += 2) {
+            consume(qa);
+            qa = load_next();
+            if (s + 1 < total) {
+                consume(qb);
+                qb = load_next();
+            }
         }
         return;
     }
@@ -476,7 +589,8 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     const int64_t rows_cta = (L->n + grid - 1) / grid;
     const int64_t waves = (rows_cta + max_warps - 1) / max_warps;
     const int warps = (int)((rows_cta + waves - 1) / waves);
-    const SmemLayout SL = smem_layout(B, (int)tc, warps, (int)ntiles);
+    const int64_t xstride = (tc + 31) / 32 * 32;  // whole 32-chunk sweeps per vector
+    const SmemLayout SL = smem_layout(B, (int)xstride, warps, (int)ntiles);
     li->grid = (int32_t)grid;
     li->block = 32 * warps;
     li->tile_chunks = (int32_t)tc;
@@ -484,6 +598,39 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     li->smem_bytes = (int32_t)SL.total;
     li->num_sms = sms;
     return WW_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// x viewed as a [B][W][32 floats] tensor (one 128-byte row per 16-column chunk); boxes of
+// 32 chunks x 128 B land 128B-swizzled, i.e. granule g of chunk tc at g ^ (tc & 7) -- the
+// layout chunk() reads.  Needs 16 | m, a 16-B aligned x and an even ldx (else cp.async).
+bool encode_x_map(Params& p, int B) {
+    if (p.m % 16 != 0 || ((uintptr_t)p.X & 15) || (B > 1 && (p.ldx % 2) != 0)) return false;
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {32, (cuuint64_t)p.W, (cuuint64_t)B};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)p.ldx * 8};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p.X), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
 template <int B>
@@ -521,6 +668,8 @@ cudaError_t launch(const Params& p, const ww_launch_info& li, int B, cudaStream_
     return cudaErrorInvalidValue;
 }
 
+bool g_force_cp_async = false;  // tests: exercise the per-thread cp.async staging path
+
 ww_status check_layer(const ww_layer* L, const char* fn) {
     if (!L) return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: null layer", fn);
     if (L->n < 1 || L->m < 1)
@@ -540,6 +689,9 @@ ww_status check_layer(const ww_layer* L, const char* fn) {
 
 }  // namespace
 
+// Not part of the ABI (no declaration in ww.h): lets the tests force the cp.async staging path.
+extern "C" void ww_debug_force_cp_async(int on) { g_force_cp_async = on != 0; }
+
 extern "C" ww_status ww_query_launch(const ww_layer* L, int32_t B, ww_launch_info* out) {
     ww_status st = check_layer(L, "ww_query_launch");
     if (st != WW_OK) return st;
@@ -549,6 +701,12 @@ extern "C" ww_status ww_query_launch(const ww_layer* L, int32_t B, ww_launch_inf
     plan(L, B, num_sms(), out);
     return ww::ok();
 }
+
+#ifdef WW_TRACE
+extern "C" int ww_debug_set_trace(void* dev_ptr) {
+    return (int)cudaMemcpyToSymbol(g_trace, &dev_ptr, sizeof(void*));
+}
+#endif
 
 extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
                                         const float* scales_d, const float* X_d, int64_t ldx,
@@ -573,6 +731,7 @@ extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
     ww_launch_info li;
     plan(L, B, num_sms(), &li);
     Params p;
+    memset(&p, 0, sizeof p);
     p.packed = reinterpret_cast<const uint4*>(packed_d);
     p.scales = scales_d;
     p.X = X_d;
@@ -588,6 +747,8 @@ extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
     p.ntiles = li.tiles;
 
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
+    p.x_stride = (li.tile_chunks + 31) / 32 * 32;
+    p.use_tma = li.tiles == 1 && !g_force_cp_async ? (encode_x_map(p, B) ? 1 : 0) : 0;
     cudaError_t e = launch(p, li, B, (cudaStream_t)stream, (L->flags & WW_FLAG_PDL) != 0);
     if (e != cudaSuccess)
         return ww::fail(WW_ERR_CUDA, "ww_wl_gemv: launch failed: %s", cudaGetErrorString(e));

@@ -197,3 +197,18 @@ def test_argument_errors_before_launch():
     with pytest.raises(ww.WWError) as e:
         ww.wl_gemv(L, case.packed_d, case.scales_d, case.x_d[0], case.x_d[0].view(torch.complex64))
     assert e.value.status == ww.ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("n,m,B", [(2048, 2048, 1), (300, 5504, 3), (77, 1000, 1)])
+def test_cp_async_staging_path_matches_tma_path(n, m, B):
+    # x staged by per-thread cp.async (fallback for 16 !| m, misaligned x, odd ldx) must give
+    # the same bits as the TMA (cp.async.bulk.tensor, 128B swizzle) staging
+    case = LayerCase(n, m, seed=n + m + B, B=B).device(ww, torch)
+    y_tma = case.gpu(ww, torch, ww.CONV_EQ1)
+    ww._lib.ww_debug_force_cp_async(1)
+    try:
+        y_cpa = case.gpu(ww, torch, ww.CONV_EQ1)
+    finally:
+        ww._lib.ww_debug_force_cp_async(0)
+    assert np.array_equal(y_tma, y_cpa)
+    assert_parity(y_cpa, case.oracle(orc.CONV_EQ1), case)

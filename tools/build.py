@@ -83,6 +83,16 @@ def build_product(force=False):
     _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs)
 
 
+def build_trace():
+    """libww_trace.so: the product sources with -DWW_TRACE (per-warp timestamps); tools only."""
+    out = os.path.join(ROOT, "build", "libww_trace.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    srcs = [s for s in product_sources() if s.endswith((".cu", ".cc"))]
+    _run([NVCC] + NVCC_FLAGS + ["-DWW_TRACE", "-I", os.path.join(ROOT, "include"), "-shared",
+                                "-o", out] + srcs)
+    return out
+
+
 def build_all(force=False):
     build_oracle(force)
     build_inputs(force)

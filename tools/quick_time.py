@@ -12,9 +12,11 @@ import paper_2604_20913_b200 as ww  # noqa: E402
 import ww_inputs as wi  # noqa: E402
 
 
-def time_shape(n, m, B=1, reps_graph=20, flags=0, l2_bytes=126 * 2**20):
+def time_shape(n, m, B=1, reps_graph=20, flags=0, l2_bytes=126 * 2**20, warm=False):
     nbytes = ww.packed_bytes(n, m)
     R = max(1, int(np.ceil(4 * l2_bytes / nbytes)))
+    if warm:  # one weight set, launched R times back to back (L2-resident)
+        R_launch, R = R, 1
     planes = torch.empty((4, n, m), dtype=torch.int8, device="cuda")
     for p in range(4):
         wi.codes_device(1, p, n, m, planes[p])
@@ -28,13 +30,14 @@ def time_shape(n, m, B=1, reps_graph=20, flags=0, l2_bytes=126 * 2**20):
     L = ww.Layer(n, m, flags=flags)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
-        for r in range(R):
-            ww.wl_gemv_batched(L, reps[r], sc, X, Y, stream=s)
+        NL = R_launch if warm else R
+        for r in range(NL):
+            ww.wl_gemv_batched(L, reps[r % R], sc, X, Y, stream=s)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            for r in range(R):
-                ww.wl_gemv_batched(L, reps[r], sc, X, Y, stream=s)
+            for r in range(NL):
+                ww.wl_gemv_batched(L, reps[r % R], sc, X, Y, stream=s)
         g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -44,7 +47,7 @@ def time_shape(n, m, B=1, reps_graph=20, flags=0, l2_bytes=126 * 2**20):
             g.replay()
             e1.record(s)
             e1.synchronize()
-            ts.append(e0.elapsed_time(e1) * 1e3 / R)
+            ts.append(e0.elapsed_time(e1) * 1e3 / NL)
     us = float(np.median(ts))
     algo = nbytes + 8 * m * B + 8 * n * B + 16 * n
     codes = 4 * n * m * B
@@ -53,6 +56,23 @@ def time_shape(n, m, B=1, reps_graph=20, flags=0, l2_bytes=126 * 2**20):
 
 if __name__ == "__main__":
     print(torch.cuda.get_device_name(), flush=True)
+    if "--scan" in sys.argv:
+        for m in (2048, 5504):
+            for k in (1, 2, 4, 8, 14, 16, 28, 32, 48):
+                n = 148 * k
+                for flags in (0, ww.FLAG_PDL):
+                    us, gbs, tcodes, R = time_shape(n, m, 1, flags=flags, warm=True)
+                    print(f"m={m} rows/SM={k:3d} pdl={flags}: {us:8.2f} us  "
+                          f"({tcodes*1e12/148/1.965e9:5.1f} codes/clk/SM)", flush=True)
+        sys.exit(0)
+    if "--warm" in sys.argv:
+        for (n, m) in ((2048, 2048), (5504, 2048), (2048, 5504)):
+            for flags in (0, ww.FLAG_PDL):
+                for warm in (False, True):
+                    us, gbs, tcodes, R = time_shape(n, m, 1, flags=flags, warm=warm)
+                    print(f"n={n} m={m} pdl={flags} {'L2-warm ' if warm else 'HBM-cold'}: {us:.2f} us "
+                          f"({tcodes*1e12/148/1.965e9:.1f} codes/clk/SM)", flush=True)
+        sys.exit(0)
     for (n, m) in ((2048, 2048), (5504, 2048), (2048, 5504)):
         for flags in (0, ww.FLAG_PDL):
             us, gbs, tcodes, R = time_shape(n, m, 1, flags=flags)

@@ -1,0 +1,57 @@
+"""Per-warp timeline of one WL-GEMV launch (build/libww_trace.so, -DWW_TRACE): globaltimer
+stamps at kernel entry (0), before/after griddepcontrol.wait (1, 2), after issuing the x
+staging (3), then at the start of every sweep and after every row's epilogue (4, 5, ...)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import build  # noqa: E402
+import paper_2604_20913_b200 as ww  # noqa: E402
+import ww_inputs as wi  # noqa: E402
+
+_tp = os.path.join(ROOT, "build", "libww_trace.so")
+lib = ctypes.CDLL(_tp if os.path.exists(_tp) else build.build_trace())
+lib.ww_debug_set_trace.argtypes = [ctypes.c_void_p]
+lib.ww_wl_gemv_batched.restype = ctypes.c_int
+lib.ww_wl_gemv_batched.argtypes = [ctypes.POINTER(ww._Layer), ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                   ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
+
+for (n, m) in [(2048, 5504), (148, 5504), (2048, 2048), (5504, 2048)]:
+    planes = torch.empty((4, n, m), dtype=torch.int8, device="cuda")
+    for p in range(4):
+        wi.codes_device(1, p, n, m, planes[p])
+    packed = ww.pack_ternary_device(planes)
+    sc = torch.rand((n, 4), device="cuda") * 0.09 + 0.01
+    X = torch.randn((1, m), dtype=torch.complex64, device="cuda")
+    Y = torch.empty((1, n), dtype=torch.complex64, device="cuda")
+    tr = torch.zeros(148 * 32 * 32, dtype=torch.int64, device="cuda")
+    L = ww.Layer(n, m).c()
+    s = torch.cuda.current_stream().cuda_stream
+    for it in range(3):
+        if it == 2:
+            lib.ww_debug_set_trace(tr.data_ptr())
+        rc = lib.ww_wl_gemv_batched(ctypes.byref(L), packed.data_ptr(), sc.data_ptr(), X.data_ptr(),
+                                    m, Y.data_ptr(), n, 1, s)
+        assert rc == 0
+        torch.cuda.synchronize()
+    lib.ww_debug_set_trace(None)
+    t = tr.cpu().numpy().reshape(148, 32, 32).astype(np.int64)
+    valid = t[:, :, 0] > 0
+    t0 = t[valid][:, 0].min()
+    rel = np.where(t > 0, t - t0, -1)
+    print(f"== n={n} m={m}: warps traced {valid.sum()}")
+    w = rel[valid]
+    for ev in range(0, 18):
+        col = w[:, ev]
+        col = col[col >= 0]
+        if col.size:
+            print(f"  ev{ev:2d}: min {col.min()/1e3:7.2f} us  median {np.median(col)/1e3:7.2f}  max {col.max()/1e3:7.2f}")
+    last = np.array([r[r >= 0].max() for r in w])
+    print(f"  last event: median {np.median(last)/1e3:.2f} us, max {last.max()/1e3:.2f} us")

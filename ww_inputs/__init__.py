@@ -98,11 +98,13 @@ def planes(seed: int, n: int, m: int, dist=LLAMA, row0: int = 0,
     return np.stack([codes(seed, p, n, m, dist, row0, nrows) for p in range(4)])
 
 
-def codes_device(seed: int, plane: int, n: int, m: int, out, dist=LLAMA, stream=None):
-    """Fill a (n, m) int8 CUDA tensor ``out`` (leading dim out.stride(0)) on the GPU."""
+def codes_device(seed: int, plane: int, n: int, m: int, out, dist=LLAMA, stream=None,
+                 row0: int = 0):
+    """Fill a (n, m) int8 CUDA tensor ``out`` (leading dim out.stride(0)) on the GPU with
+    rows row0 .. row0+n of the plane (same values as ``codes(..., row0=row0)``)."""
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
-    rc = _devlib().wwi_gen_codes_device(seed, plane, m, 0, n, dist[0], dist[1],
+    rc = _devlib().wwi_gen_codes_device(seed, plane, m, row0, n, dist[0], dist[1],
                                         out.data_ptr(), out.stride(0), s.cuda_stream)
     if rc != 0:
         raise RuntimeError("wwi_gen_codes_device failed")
