@@ -22,6 +22,22 @@ from . import (CONV_EQ1, FLAG_PDL, LAYOUT_COL4, SCALES_PER_ROW, Layer, packed_by
 PROJ_NAMES = ("q", "k", "v", "o", "gate", "up", "down")
 
 
+def exchange_shards(y, rank: int, world: int, group=None):
+    """In-place all-gather of a rank-major gathered buffer y ([world][B][rows_per_rank]
+    flattened): this rank's slot is the input, every rank ends with all slots (ww.h
+    ww_shard_plan).  NCCL on GPUs, gloo on CPU (tests)."""
+    if world == 1:
+        return
+    import torch.distributed as dist
+    n = y.numel() // world
+    dist.all_gather_into_tensor(y, y[rank * n:(rank + 1) * n], group=group)
+
+
+def gathered_rows(y, world: int, B: int, rows_per_rank: int, n: int, b: int = 0):
+    """Rows 0..n-1 of vector b from a rank-major gathered buffer."""
+    return y.view(world, B, rows_per_rank)[:, b, :].reshape(-1)[:n]
+
+
 @dataclass
 class Proj:
     layer: int
@@ -99,9 +115,8 @@ class WLStack:
 
     def gathered(self, pr: Proj, b: int = 0):
         """Full output y[b] (n rows) of a projection after the all-gather."""
-        rpr = pr.shard.rows_per_rank
-        yy = self.Y[self.projs.index(pr)].view(self.world, self.B, rpr)[:, b, :].reshape(-1)
-        return yy[:pr.spec.n]
+        return gathered_rows(self.Y[self.projs.index(pr)], self.world, self.B,
+                             pr.shard.rows_per_rank, pr.spec.n, b)
 
     # ------------------------------------------------------------------ the step
     def launch(self, i: int, stream=None):
@@ -118,18 +133,17 @@ class WLStack:
         """All-gather of projection i's y shards (NCCL over NVLink); no-op on one rank."""
         if self.world == 1:
             return 0
-        import torch.distributed as dist
-        y = self.Y[i]
-        n = y.numel() // self.world
-        dist.all_gather_into_tensor(y, y[self.rank * n:(self.rank + 1) * n], group=self.group)
+        exchange_shards(self.Y[i], self.rank, self.world, self.group)
         return 1
 
-    def step(self, stream=None):
-        """One token through the whole stack; returns the number of WL-GEMV launches."""
+    def step(self, stream=None, exchange: bool = True):
+        """One token through the whole stack; returns the number of WL-GEMV launches.
+        exchange=False skips the all-gathers (tests emulating ranks on one GPU)."""
         k = 0
         for i in range(len(self.projs)):
             k += self.launch(i, stream)
-            self.exchange(i)
+            if exchange:
+                self.exchange(i)
         return k
 
     # ------------------------------------------------------------------ accounting
