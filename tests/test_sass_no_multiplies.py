@@ -1,0 +1,64 @@
+"""App. D on B200: the hot loop of the shipped sm_100a kernel contains no
+floating-point multiply.  Disassembles libww.so with cuobjdump (CPU only) and inspects
+the instructions between the first and last packed-fp32 add of the B = 1 kernel's
+accumulation loop; the only FMULs allowed are the 8 scale multiplies of the epilogue,
+which sit outside that region."""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_2604_20913_b200", "libww.so")
+FP_MUL = re.compile(r"\b(FMUL2?|FFMA2?|DMUL|DFMA|HMUL2|FMUL32I|FFMA32I)\b")
+
+
+def _kernel_sass(name_pat):
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+    funcs = re.split(r"\n\s*Function : ", out)
+    for f in funcs:
+        if re.match(name_pat, f):
+            return [ln.split(";")[0].strip() for ln in f.splitlines() if re.search(r"/\*[0-9a-f]{4}\*/", ln)]
+    pytest.fail(f"kernel {name_pat} not found in {LIB}")
+
+
+def _strip(ln):
+    return re.sub(r"^/\*[0-9a-f]+\*/\s*", "", ln)
+
+
+@pytest.mark.parametrize("B", [1, 4])
+def test_accumulation_loop_has_no_fp_multiply(B):
+    sass = [_strip(l) for l in _kernel_sass(rf"_ZN\S*wl_gemv_kernelILi{B}EE")]
+    # accumulation blocks: maximal runs of predicated FADD2 (Eqs. 6-7 as predicated packed
+    # adds) no more than 12 instructions apart -- one block per unrolled 64-code chunk body
+    idx = [i for i, l in enumerate(sass) if re.match(r"@!?P\d\s+FADD2\b", l)]
+    blocks, start = [], idx[0]
+    for a, b in zip(idx, idx[1:] + [None]):
+        if b is None or b - a > 12:
+            blocks.append((start, a))
+            start = b
+    big = [(a, b) for a, b in blocks if sum(1 for i in idx if a <= i <= b) >= 128 * B]
+    assert big, "expected a block of >= 128*B predicated FADD2 (64 codes x 2 per chunk)"
+    for a, b in big:
+        region = sass[a:b + 1]
+        bad = [l for l in region if FP_MUL.search(l)]
+        # HFMA2 Rx, -RZ, RZ, c, c is ptxas' constant-materialisation idiom, not a multiply
+        bad += [l for l in region if re.search(r"\bHFMA2\b", l) and "-RZ, RZ" not in l]
+        assert not bad, bad[:5]
+
+
+def test_scale_multiplies_exist_only_in_epilogue():
+    sass = [_strip(l) for l in _kernel_sass(r"_ZN\S*wl_gemv_kernelILi1EE")]
+    fmul = [i for i, l in enumerate(sass) if re.search(r"\bFMUL\b", l)]
+    fadd2 = [i for i, l in enumerate(sass) if re.match(r"@!?P\d\s+FADD2\b", l)]
+    assert fmul, "the epilogue's scale multiplies (P:1002-1011) should be FMULs"
+    # every FMUL lies outside the [first, last] span of some contiguous accumulation block:
+    # i.e. no FMUL between two predicated FADD2 that are within 8 instructions of each other
+    for i in fmul:
+        before = [j for j in fadd2 if j < i]
+        after = [j for j in fadd2 if j > i]
+        assert not (before and after and after[0] - before[-1] <= 8), sass[i]
