@@ -2,8 +2,9 @@
 
 Default workload (BASELINE.json config 4, the 7B decode linear stack): one step = one token
 through 32 decoder layers x 7 widely-linear projections (q,k,v,o 2048->2048; gate,up
-2048->5504; down 5504->2048, complex), B = 1, every projection's output rows sharded over
-the GPUs and all-gathered (NCCL).  The 1.62 GB of packed weights per step is > 12x L2, so
+2048->5504; down 5504->2048, complex), B = 1, launched as 4 stages per layer (q/k/v and
+gate/up share their input, so each group is one launch), every stage's output rows sharded
+over the GPUs and all-gathered (NCCL).  The 1.62 GB of packed weights per step is > 12x L2, so
 every step streams its weights from HBM (no flush needed).
 
     python bench.py [--gpus N --steps K --warmup W] [--workload c4|c2|c3a|c3b|c5] [--batch B]
@@ -186,10 +187,12 @@ def run_ours(args, world, rank, local):
 
     if args.workload == "c4":
         stack = WLStack(layers=args.layers, seed=args.seed, B=args.batch, rank=rank, world=world,
-                        pdl=not args.no_pdl, device=dev, group=group)
+                        pdl=not args.no_pdl, device=dev, group=group, fuse=not args.no_fuse)
         units = [stack]
-        layers_per_step = len(stack.projs)
-        workload = f"c4_llama2_7b_wl_decode_stack ({args.layers} layers x 7 projections)"
+        layers_per_step = 7 * args.layers  # widely-linear projections per token
+        workload = (f"c4_llama2_7b_wl_decode_stack ({args.layers} layers x 7 projections, "
+                    + ("q/k/v and gate/up launched together per shared input: 4 launches per "
+                       "layer" if not args.no_fuse else "one launch per projection") + ")")
     else:
         # single-layer configs: R replicas of the layer (>= 4x L2) cycled inside a step
         spec = {"c2": wi.C2, "c3a": wi.C3A, "c3b": wi.C3B, "c5": wi.C3B, "c1": wi.C1}[args.workload]
@@ -268,10 +271,12 @@ def run_ours(args, world, rank, local):
     per_shape = {}
     kern_ms_total = 0.0
     if args.workload == "c4":
-        for p_idx, key in ((0, "q/k/v/o"), (4, "gate/up"), (6, "down")):
-            idx = [i for i, pr in enumerate(stack.projs) if pr.proj == p_idx]
-            pr0 = stack.projs[idx[0]]
-            label = f"{key} {pr0.ylocal}x{pr0.spec.m}"
+        kinds = {}
+        for i, st in enumerate(stack.stages):
+            kinds.setdefault(st.name, []).append(i)
+        for name, idx in kinds.items():
+            st0 = stack.stages[idx[0]]
+            label = f"{name} {st0.ylocal}x{st0.m}"
             try:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.stream(s):
@@ -291,9 +296,7 @@ def run_ours(args, world, rank, local):
                     b.record(s)
                 torch.cuda.synchronize(dev)
                 per_shape[label] = round(a.elapsed_time(b) * 1e3 / (5 * len(idx)), 3)
-                kern_ms_total += per_shape[label] * 1e-3 * sum(
-                    1 for pr in stack.projs if pr.proj in
-                    ({0: (0, 1, 2, 3), 4: (4, 5), 6: (6,)}[p_idx]))
+                kern_ms_total += per_shape[label] * 1e-3 * len(idx)
             except Exception as e:  # pragma: no cover
                 per_shape[label] = f"unavailable: {e!r}"
 
@@ -347,6 +350,7 @@ def run_ours(args, world, rank, local):
                          if args.workload == "c4" else "rotating replicas >= 4x L2",
                    "launch": ww.query_launch(ww.Layer(2048, 5504), args.batch)},
         "us_per_layer": round(1e3 * ms_step / layers_per_step, 3),
+        "launches_per_step": launches_per_step,
         "per_shape_us": per_shape,
         "pct_of_hbm_peak": round(100 * (pa_bytes / (ms_step * 1e-3) / 1e9) / world
                                  / peaks.get("hbm_gbs", 6650.0), 2),
@@ -468,6 +472,8 @@ def main():
     ap.add_argument("--workload", choices=("c4", "c1", "c2", "c3a", "c3b", "c5"), default="c4")
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--no-fuse", action="store_true",
+                    help="c4: one launch per projection instead of one per shared input")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")

@@ -14,7 +14,9 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libww.so")
+# WW_LIB_OVERRIDE: development tools only (A/B timing of kernel variants built from the same
+# sources with other -D flags); the tests, smoke() and bench.py always load the in-tree build
+LIB_PATH = os.environ.get("WW_LIB_OVERRIDE") or os.path.join(_HERE, "libww.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
@@ -58,7 +60,8 @@ class _Shard(ctypes.Structure):
 
 class _LaunchInfo(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in ("grid", "block", "smem_bytes", "tiles",
-                                              "tile_chunks", "num_sms")]
+                                              "tile_chunks", "num_sms", "parts", "split_chunks",
+                                              "ring_slots")]
 
 
 _i64, _i32, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p

@@ -29,9 +29,17 @@
 namespace {
 
 // warps per CTA: 16 while the B accumulators leave room, 8 (255-register cap) above
+// warps per CTA, a multiple of 4 so the four SM sub-partitions get equal warps: 16 while
+// the B accumulators leave room, 8 (255-register cap) above
 template <int B>
 __host__ __device__ constexpr int warps_for() { return B <= 4 ? 16 : 8; }
+inline int warps_for_b(int B) { return B <= 4 ? 16 : 8; }
 constexpr int kXBudgetBytes = 184 * 1024;  // x tile per CTA (one CTA per SM)
+constexpr int kMaxRing = 8;                // weight-ring slots per warp (512 B each)
+#ifndef WW_WEIGHT_RING
+#define WW_WEIGHT_RING 0  // 1: per-warp TMA bulk rings in shared memory (A/B builds; measured
+                          // ~4% slower than the two-sweep register prefetch)
+#endif
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
@@ -57,6 +65,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int sr
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, int src_bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
                  : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
@@ -94,8 +105,17 @@ struct alignas(64) Params {
     float* Y;             // B x ldy complex64
     int64_t n, m, W, ldx, ldy;
     int32_t per_row_scales, conv, tile_chunks, ntiles, aligned16;
-    int32_t x_stride;     // chunks per vector in the shared x tile (multiple of 32)
+    int32_t x_stride;     // multi-tile path: chunks per vector in the shared x tile
     int32_t use_tma;      // stage x with cp.async.bulk.tensor (else per-thread cp.async)
+    int32_t parts;        // single-tile path: column parts per row (1 or 2), see plan()
+    int32_t split;        // chunks of part 0 (== W when parts == 1)
+    int32_t J0, J1;       // 32-chunk sweeps (= x slices) of part 0 and part 1
+    int32_t ring;         // single-tile path: weight-ring slots (one 512-B sweep each) per warp
+    int32_t scale_rows;   // single-tile path: per-CTA row capacity of the shared scale copy
+                          // (0: the epilogue reads scales from global memory)
+    int32_t dbg;          // tools only (ww_debug_set_flags): 1 = skip griddepcontrol.wait,
+                          // 2 = skip the accumulation, 8 = bulk L2 prefetch of the CTA's
+                          // weights at kernel start (overhead measurement); 0 in the product
 };
 
 __host__ __device__ constexpr int next_pow2(int v) {
@@ -129,93 +149,130 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void mbar_wait0(uint32_t bar) {
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t done;
     do {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(bar)
+            : "r"(bar), "r"(parity)
             : "memory");
     } while (!done);
 }
+__device__ __forceinline__ void mbar_wait0(uint32_t bar) { mbar_wait(bar, 0); }
 
-// Issue the cp.async copies of x columns of chunks [c0 + tc_lo, c0 + tc_hi) for all B vectors
+// TMA bulk copy (cp.async.bulk, no tensor map) of `bytes` (multiple of 16) from global
+// memory into shared memory, completing on mbarrier `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint4 lds128u(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
+
+// cp.async of one 16-byte x granule (columns col, col+1 of vector row `src`), zero-filling
+// columns >= m (R6)
+__device__ __forceinline__ void stage_granule(const Params& p, uint32_t dst, const float* src,
+                                              int64_t valid) {
+    if (p.aligned16) {
+        const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
+        cp_async16(dst, bytes ? (const void*)src : (const void*)p.X, bytes);
+    } else {
+        cp_async8(dst, valid >= 1 ? (const void*)src : (const void*)p.X, valid >= 1 ? 8 : 0);
+        cp_async8(dst + 8, valid >= 2 ? (const void*)(src + 2) : (const void*)p.X,
+                  valid >= 2 ? 8 : 0);
+    }
+}
+
+// Multi-tile path: cp.async copies of x columns of chunks [c0, c0 + tc_n) for all B vectors
 // into the swizzled tile: granule g (columns 2g, 2g+1) of tile chunk tc lives at
-// ((b*TC + tc)*8 + (g ^ (tc&7)))*16, so 32 lanes reading 32 consecutive chunks hit 32 banks.
-// Columns >= m are zero-filled (R6).
+// ((b*XS + tc)*8 + (g ^ (tc&7)))*16, so 32 lanes reading 32 consecutive chunks hit 32 banks.
 template <int B>
-__device__ __forceinline__ void stage_x(const Params& p, uint32_t xs, int64_t c0, int tc_lo,
-                                        int tc_hi) {
+__device__ __forceinline__ void stage_x(const Params& p, uint32_t xs, int64_t c0, int tc_n) {
     const int XS = p.x_stride;
-    const int span8 = (tc_hi - tc_lo) * 8;
+    const int span8 = tc_n * 8;
 #pragma unroll 1
     for (int b = 0; b < B; ++b) {
-        const float* xb = p.X + 2 * (b * p.ldx + (c0 + tc_lo) * 16);
-        const int64_t left0 = p.m - (c0 + tc_lo) * 16;  // valid columns from the slice start
-        const uint32_t base = xs + (uint32_t)((b * XS + tc_lo) * 128);
+        const float* xb = p.X + 2 * (b * p.ldx + c0 * 16);
+        const uint32_t base = xs + (uint32_t)(b * XS * 128);
         for (int g = threadIdx.x; g < span8; g += blockDim.x) {
-            const int tcl = g >> 3, gg = g & 7;  // tile chunk (relative), granule
-            const int64_t valid = left0 - 2 * g;   // columns left at this granule
-            const float* src = xb + 4 * g;
-            const uint32_t dst = base + (uint32_t)((tcl * 8 + (gg ^ ((tc_lo + tcl) & 7))) * 16);
-            if (p.aligned16) {
-                const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
-                cp_async16(dst, bytes ? (const void*)src : (const void*)p.X, bytes);
-            } else {
-                cp_async8(dst, valid >= 1 ? (const void*)src : (const void*)p.X, valid >= 1 ? 8 : 0);
-                cp_async8(dst + 8, valid >= 2 ? (const void*)(src + 2) : (const void*)p.X,
-                          valid >= 2 ? 8 : 0);
-            }
-        }
-    }
-}
-
-// Single-tile staging of all of x, sliced for early start: granules (16 B = 2 columns) are
-// numbered g = (b*TC + tc)*8 + gg; slice j = 32-chunk sweep j of every vector completes
-// mbarrier j.  Each thread issues its granules in slice order and arrives on barrier j once
-// all of its slice-<=j copies are issued (cp.async.mbarrier.arrive fires when they land).
-template <int B>
-__device__ __forceinline__ void stage_x_sliced(const Params& p, uint32_t xs, uint32_t bars,
-                                               int J) {
-    const int TC = p.tile_chunks, XS = p.x_stride;
-    const int per_b = TC * 8;  // granules per vector
-    int next = 0;              // next slice barrier to arrive on
-    // iterate slice-major so a thread's copies are issued in slice order
-    for (int j = 0; j < J; ++j) {
-        const int g_lo = 256 * j, g_hi = (256 * j + 256 < per_b ? 256 * j + 256 : per_b);
-        const int span = g_hi - g_lo;
-        for (int t = threadIdx.x; t < B * span; t += blockDim.x) {
-            const int b = B == 1 ? 0 : t / span;
-            const int g = g_lo + (B == 1 ? t : t - b * span);
             const int tc = g >> 3, gg = g & 7;
-            const int64_t col = (int64_t)tc * 16 + 2 * gg;
-            const int64_t valid = p.m - col;
-            const float* src = p.X + 2 * (b * p.ldx + col);
-            const uint32_t dst = xs + (uint32_t)(((b * XS + tc) * 8 + (gg ^ (tc & 7))) * 16);
-            if (p.aligned16) {
-                const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
-                cp_async16(dst, bytes ? (const void*)src : (const void*)p.X, bytes);
-            } else {
-                cp_async8(dst, valid >= 1 ? (const void*)src : (const void*)p.X, valid >= 1 ? 8 : 0);
-                cp_async8(dst + 8, valid >= 2 ? (const void*)(src + 2) : (const void*)p.X,
-                          valid >= 2 ? 8 : 0);
-            }
+            const uint32_t dst = base + (uint32_t)((tc * 8 + (gg ^ (tc & 7))) * 16);
+            stage_granule(p, dst, xb + 4 * g, p.m - (c0 * 16 + 2 * g));
         }
-        cp_async_arrive(bars + 8 * next);
-        ++next;
     }
 }
 
-// Accumulators: S column-parity sets of B x 4 pair sums.  For B <= 2 even and odd columns
-// feed separate sets (more independent FADD2 chains per warp, half-length fp32 chains);
-// larger B has ILP across vectors.  N = 2 would keep separate positive / negative sums
-// (acc = pos - neg); measured no faster on B200, so N = 1.
+// Single-tile x staging.  Part h of the row (chunks [lo_h, lo_h + len_h)) has its own x
+// region at xs + roff_h: vector b's 32*J_h chunks at + b*J_h*4096, chunk c (relative to lo_h)
+// at + c*128, granules swizzled by (c & 7) -- the 128B-swizzle TMA layout, since every
+// region is 1024-B aligned.  Slice j of part h = relative chunks [32j, 32j+32) of every
+// vector, completing mbarrier h*J0 + j.  Slices are issued interleaved (part 0 slice j,
+// part 1 slice j, ...) so the warps that start on part 1 do not wait for all of part 0.
+template <int B>
+__device__ __forceinline__ void stage_x_regions_cp_async(const Params& p, uint32_t xs,
+                                                         uint32_t bars) {
+    const int jmax = p.J0 > p.J1 ? p.J0 : p.J1;
+    for (int j = 0; j < jmax; ++j) {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int Jh = h ? p.J1 : p.J0, lo = h ? p.split : 0;
+            const uint32_t roff = h ? (uint32_t)(B * p.J0 * 4096) : 0u;
+            if (j >= Jh) continue;
+            const int span = 32 * 8;  // granules per vector in one slice
+            for (int t = threadIdx.x; t < B * span; t += blockDim.x) {
+                const int b = B == 1 ? 0 : t / span;
+                const int g = 32 * 8 * j + (B == 1 ? t : t - b * span);
+                const int tc = g >> 3, gg = g & 7;  // chunk relative to the part
+                const int64_t col = (int64_t)(lo + tc) * 16 + 2 * gg;
+                const uint32_t dst = xs + roff +
+                                     (uint32_t)(((b * Jh * 32 + tc) * 8 + (gg ^ (tc & 7))) * 16);
+                stage_granule(p, dst, p.X + 2 * (b * p.ldx + col), p.m - col);
+            }
+            cp_async_arrive(bars + 8 * (h * p.J0 + j));
+        }
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void stage_x_regions_tma(const Params& p, uint32_t xs, uint32_t bars) {
+    const int jmax = p.J0 > p.J1 ? p.J0 : p.J1;
+    for (int j = 0; j < jmax; ++j) {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int Jh = h ? p.J1 : p.J0, lo = h ? p.split : 0;
+            const uint32_t roff = h ? (uint32_t)(B * p.J0 * 4096) : 0u;
+            if (j >= Jh) continue;
+            const uint32_t bar = bars + 8 * (h * p.J0 + j);
+            mbar_expect_tx(bar, (uint32_t)(B * 4096));
+#pragma unroll 1
+            for (int b = 0; b < B; ++b)
+                tma_load_3d(xs + roff + (uint32_t)((b * Jh + j) * 4096), &p.tmap, 0, lo + 32 * j,
+                            b, bar);
+        }
+    }
+}
+
+// Accumulators: S column-parity sets of B x 4 pair sums (N = 2: separate sums of the +1 and
+// the -1 codes, combined as pos - neg at the end).  For B <= 2 even and odd columns feed
+// separate sets (more independent FADD2 chains per warp, half-length fp32 chains); larger
+// B has ILP across vectors.
+#ifndef WW_ACC_N
+#define WW_ACC_N 1
+#endif
 template <int B>
 struct Acc {
     static constexpr int S = B <= 2 ? 2 : 1;  // column-parity sets
-    static constexpr int N = 1;
+    static constexpr int N = WW_ACC_N;
     float2 a[S][N][B][4];
     __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -227,7 +284,7 @@ struct Acc {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) a[s][k][b][q] = make_float2(0.f, 0.f);
     }
-    // sum over sets of plane q, vector b: pos - neg
+    // sum over sets of plane q, vector b (pos - neg when N == 2)
     __device__ __forceinline__ float2 total(int b, int q) const {
         float2 t = a[0][0][b][q];
         if (S == 2) t = fadd2(t, a[S - 1][0][b][q]);
@@ -282,7 +339,9 @@ __device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xc, u
 }
 
 // Transpose-reduce NV (power of 2) partial sums across the warp: after the halving rounds
-// lane l holds NV>>H totals starting at index (bit4(l) bit3(l) ...)_2 * (NV>>H).
+// lane l holds NV>>H totals starting at index (bit4(l) bit3(l) ...)_2 * (NV>>H).  Every
+// value is summed over the lanes in the same xor-butterfly order (16, 8, 4, 2, 1) for any
+// NV, so the totals do not depend on how many values are reduced together.
 template <int NV>
 __device__ __forceinline__ void warp_transpose_reduce(float (&v)[NV]) {
     const int lane = threadIdx.x & 31;
@@ -336,14 +395,18 @@ __device__ __forceinline__ void reduce_to(const Acc<B>& acc, float* dst) {
     __syncwarp();
 }
 
-// Epilogue (a8): lane b < B applies the row's 8 scales once to the totals T
-// of vector b and stores y.
+// Epilogue (a8): lane b < B forms the row totals of vector b (part 0, plus part 1 when the
+// row has two parts: T = T0 + T1 in that order), applies the row's 8 scales once
+// (s = the row's [sUr, sUi, sWr, sWi], staged in shared memory when they fit)
+// and stores y.
 template <int B>
-__device__ __forceinline__ void epilogue(const Params& p, const float* T0, int64_t row) {
+__device__ __forceinline__ void epilogue(const Params& p, const float* T0, const float* T1,
+                                         int64_t row, const float* s) {
     const int lane = threadIdx.x & 31;
     if (lane < B) {
-        const float* T = T0 + 8 * lane;
-        const float* s = p.scales + (p.per_row_scales ? 4 * row : 0);
+        float T[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) T[i] = T1 ? T0[8 * lane + i] + T1[8 * lane + i] : T0[8 * lane + i];
         const float sUr = s[0], sUi = s[1], sWr = s[2], sWi = s[3];
         const float yre = sUr * T[0] - sUi * T[3] + sWr * T[4] + sWi * T[7];          // Eq. 2
         const float yim = p.conv == WW_CONV_EQ1
@@ -356,18 +419,26 @@ __device__ __forceinline__ void epilogue(const Params& p, const float* T0, int64
 
 // Shared-memory carve-up (bytes), identical on host (plan) and device.
 struct SmemLayout {
-    int64_t x_bytes, scratch_off, bar_off, total;
+    int64_t x_bytes, scratch_off, slot_off, cnt_off, scale_off, bar_off, rbar_off, ring_off, total;
 };
-// x tile first (1024-B aligned for the 128B-swizzled TMA boxes), then the per-warp reduction
-// scratch, then one mbarrier per 32-chunk x slice (single-tile launches)
-__host__ __device__ inline SmemLayout smem_layout(int B, int XS, int warps, int ntiles) {
+// x first (1024-B aligned for the 128B-swizzled TMA boxes), then per-warp reduction scratch
+// (2 parts), then -- single tile only -- the split-row slots and counters, one mbarrier per
+// x slice, one mbarrier per weight-ring slot and the per-warp weight rings (K slots of one
+// 32-chunk sweep = 512 B each).  Single tile: x_chunks = 32*(J0+J1) per vector; multi-tile:
+// the tile width.
+__host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
+                                                  int nbars, int ring, int scale_rows) {
     const int64_t nv = next_pow2(8 * B);
     SmemLayout L;
-    L.x_bytes = (int64_t)B * XS * 128;
+    L.x_bytes = (int64_t)B * x_chunks * 128;
     L.scratch_off = L.x_bytes;
-    L.bar_off = L.scratch_off + (int64_t)warps * nv * 4;
-    const int64_t nbars = ntiles == 1 ? XS / 32 : 0;
-    L.total = L.bar_off + 8 * nbars + 1024;  // + alignment slack of the dynamic smem base
+    L.slot_off = L.scratch_off + (int64_t)warps * 2 * nv * 4;
+    L.cnt_off = L.slot_off + (single ? (int64_t)(warps + 1) * 2 * nv * 4 : 0);
+    L.scale_off = L.cnt_off + (single ? ((int64_t)(warps + 1) * 4 + 15) / 16 * 16 : 0);
+    L.bar_off = L.scale_off + (single ? 16 * (int64_t)scale_rows : 0);
+    L.rbar_off = L.bar_off + (single ? 8 * (int64_t)nbars : 0);
+    L.ring_off = (L.rbar_off + (single ? 8 * (int64_t)warps * ring : 0) + 127) / 128 * 128;
+    L.total = L.ring_off + (single ? (int64_t)warps * ring * 512 : 0) + 1024;  // + base slack
     return L;
 }
 
@@ -384,29 +455,35 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t xs = (raw + 1023u) & ~1023u;  // 1024-B aligned x tile
     unsigned char* smem = smem_raw + (xs - raw);
-    const int TC = p.tile_chunks;
     const int nwarps = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int J = (TC + 31) / 32;  // lane sweeps per tile
-    const SmemLayout SL = smem_layout(B, p.x_stride, nwarps, p.ntiles);
-    float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * NV;
+    const bool single = p.ntiles == 1;
+    const int nbars = single ? p.J0 + p.J1 : 0;
+    const SmemLayout SL = smem_layout(B, single ? 32 * (p.J0 + p.J1) : p.x_stride, nwarps,
+                                      single, nbars, p.ring, p.scale_rows);
+    float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * 2 * NV;
     const uint32_t bars = xs + (uint32_t)SL.bar_off;
 
-    // balanced contiguous row range of this CTA (A12 row-parallel decomposition);
-    // the host sizes the CTA so its rows split into equal waves over its warps
+    // balanced contiguous row range of this CTA (A12 row-parallel decomposition)
     const int64_t r0 = (int64_t)blockIdx.x * p.n / gridDim.x;
     const int64_t r1 = (int64_t)(blockIdx.x + 1) * p.n / gridDim.x;
-    const bool single = p.ntiles == 1;
-    if (single && threadIdx.x == 0) {
-        for (int j = 0; j < J; ++j) mbar_init(bars + 8 * j, p.use_tma ? 1u : blockDim.x);
+    if (single) {
+        int* cnt = reinterpret_cast<int*>(smem + SL.cnt_off);
+        for (int i = threadIdx.x; i <= nwarps; i += blockDim.x) cnt[i] = 0;
+        // one mbarrier per thread (an init is a shared-memory atomic: a serial loop over the
+        // ~150 barriers costs microseconds); x-slice barriers first, then the ring barriers,
+        // which sit right after them
+        const int nrb = nwarps * p.ring;
+        for (int j = threadIdx.x; j < nbars + nrb; j += blockDim.x)
+            mbar_init(bars + 8 * j, j < nbars ? (p.use_tma ? 1u : blockDim.x) : 1u);
         fence_barrier_init();
     }
 
-    // PDL: let the next kernel launch now and warm L2 with this CTA's weights (never written
-    // by other kernels) before waiting for the producer of x / consumer of y.
+    // PDL: let the next kernel launch now.  (A bulk L2 prefetch of the CTA's weights here
+    // measured slower -- it competes with the running layer's stream; tools only: dbg & 8.)
     trace(0);
     pdl_launch_dependents();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && (p.dbg & 8)) {
         const char* wb = reinterpret_cast<const char*>(p.packed + r0 * p.W);
         const int64_t bytes = (r1 - r0) * p.W * 16;
         for (int64_t off = 0; off < bytes; off += 65536)
@@ -418,84 +495,197 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     uint32_t off[8];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) off[kk] = (uint32_t)((kk ^ (lane & 7)) << 4);
-    const uint32_t bstride = (uint32_t)p.x_stride * 128u;
 
     if (single) {
-        // This warp's rows r0 + warp + k*nwarps, each swept in J steps of 32 chunks (lane =
-        // chunk within the step; the last step has `lastw` active lanes).  The weights stream
-        // two steps ahead in registers across row boundaries; all loop state is incremental.
-        const int lastw = TC - 32 * (J - 1);
-        const int64_t myrows = r0 + warp < r1 ? (r1 - r0 - warp + nwarps - 1) / nwarps : 0;
-        const uint4* pf = p.packed + (r0 + warp) * p.W + lane;  // prefetch pointer
-        const int64_t row_jump = (int64_t)nwarps * p.W - 32 * J;
-        int64_t pf_rows = myrows;
-        int pf_j = 0;
+        // Work units: row r of the CTA is split into P = p.parts column parts
+        // (a function of m and B only, so a row's arithmetic never depends on n, the shard
+        // or the launch shape); unit u = (row u/P, part u%P).  The CTA's NR*P units are cut
+        // into contiguous per-warp ranges whose sizes differ by at most one, the longer ones
+        // on warps 0..e-1, so the four SM sub-partitions (warp % 4) get equal work.  A part
+        // is swept in 32-chunk steps (lane = chunk within the step); the warp reduces each
+        // part to 8B totals and the row total is part 0 + part 1.  A row whose parts land on
+        // two warps (at most one per warp boundary) meets in a shared-memory slot.
+        // Unit indices are relative to the CTA (int32: n <= 2^30, check_layer).
+        const int P = p.parts;
+        const int U = (int)(r1 - r0) * P;
+        const int ub = U / nwarps, ue = U - ub * nwarps;
+        const int u0 = warp * ub + (warp < ue ? warp : ue);
+        const int u1 = u0 + ub + (warp < ue ? 1 : 0);
+        const int plen1 = (int)p.W - p.split;  // chunks of part 1
+        // this warp's sweeps: part-1 units are the odd u when P == 2
+        const int n1 = P == 2 ? (u1 >> 1) - (u0 >> 1) : 0;
+        const int total = (u1 - u0 - n1) * p.J0 + n1 * p.J1;
+
+        // Weight stream (a4): each warp owns a ring of K = p.ring shared-memory slots, one
+        // 32-chunk sweep (512 contiguous bytes of a row) per slot, filled by its lane 0 with
+        // TMA bulk copies (cp.async.bulk, one mbarrier per slot).  The first K sweeps are
+        // requested before griddepcontrol.wait -- weights never depend on the previous kernel
+        // -- so they stream in while the previous layer still computes.
+        // the CTA's row scales -> shared memory (cp.async, before griddepcontrol.wait: scales
+        // are weights), so no epilogue waits on a global load
+        const bool staged = p.scale_rows > 0;
+        const float* ssm = reinterpret_cast<const float*>(smem + SL.scale_off);
+        if (staged) {
+            const int ns = p.per_row_scales ? 4 * (int)(r1 - r0) : 4;
+            const float* src = p.scales + (p.per_row_scales ? 4 * r0 : 0);
+            const uint32_t dst = xs + (uint32_t)SL.scale_off;
+            for (int i = threadIdx.x; i < ns; i += blockDim.x) cp_async4(dst + 4u * i, src + i);
+            cp_async_wait_all();  // this thread's copies; the __syncthreads below publishes them
+        }
+        auto srow = [&](int64_t row) -> const float* {
+            return staged ? ssm + (p.per_row_scales ? 4 * (row - r0) : 0)
+                          : p.scales + (p.per_row_scales ? 4 * row : 0);
+        };
+#if WW_WEIGHT_RING
+        const int K = p.ring;
+        const uint32_t ring = xs + (uint32_t)SL.ring_off + (uint32_t)(warp * K * 512);
+        const uint32_t rbar = xs + (uint32_t)SL.rbar_off + (uint32_t)(warp * K * 8);
+#endif
+        int pu = u0, pk = 0, pJ = 1, plen = 0;  // producer position (unit, sweep)
+        const uint4* pf = p.packed;
+        auto p_setup = [&]() {
+            const int h = P == 2 ? (pu & 1) : 0;
+            const int64_t row = r0 + (P == 2 ? (pu >> 1) : pu);
+            pJ = h ? p.J1 : p.J0;
+            plen = h ? plen1 : p.split;
+            pf = p.packed + row * p.W + (h ? p.split : 0);
+            pk = 0;
+        };
+        if (pu < u1) p_setup();
+#if WW_WEIGHT_RING
+        auto issue = [&](int slot) {  // the producer's next sweep into ring slot `slot`
+            if (lane == 0) {
+                const int nch = plen - 32 * pk < 32 ? plen - 32 * pk : 32;
+                const uint32_t bar = rbar + 8u * (uint32_t)slot;
+                mbar_expect_tx(bar, (uint32_t)nch * 16u);
+                bulk_g2s(ring + 512u * (uint32_t)slot, pf + 32 * pk, (uint32_t)nch * 16u, bar);
+            }
+            if (++pk == pJ) {
+                ++pu;
+                if (pu < u1) p_setup();
+            }
+        };
+        __syncthreads();  // mbarrier inits and slot counters visible
+        {
+            const int pre = total < K ? total : K;
+            for (int j = 0; j < pre; ++j) issue(j);
+        }
+#else
+        // register variant: the next two sweeps in registers (lanes past the end load zeros)
         auto load_next = [&]() -> uint4 {
             uint4 w = make_uint4(0, 0, 0, 0);
-            if (pf_rows > 0 && (pf_j < J - 1 || lane < lastw)) w = ldg_stream(pf);
-            pf += 32;
-            if (++pf_j == J) {
-                pf_j = 0;
-                pf += row_jump;
-                --pf_rows;
+            if (pu < u1 && lane < plen - 32 * pk) w = ldg_stream(pf + 32 * pk + lane);
+            if (++pk == pJ) {
+                ++pu;
+                if (pu < u1) p_setup();
             }
             return w;
         };
         uint4 qa = load_next(), qb = load_next();
-        __syncthreads();  // mbarrier inits visible
+        __syncthreads();  // mbarrier inits and slot counters visible
+#endif
         trace(1);
-        pdl_wait();
+        if (!(p.dbg & 1)) pdl_wait();
         trace(2);
-        if (p.use_tma) {  // one thread: a 4 KB 128B-swizzled box per slice and vector
-            if (threadIdx.x == 0) {
-                for (int j = 0; j < J; ++j) {
-                    mbar_expect_tx(bars + 8 * j, (uint32_t)(B * 4096));
-#pragma unroll 1
-                    for (int b = 0; b < B; ++b)
-                        tma_load_3d(xs + (uint32_t)((b * p.x_stride + 32 * j) * 128), &p.tmap, 0,
-                                    32 * j, b, bars + 8 * j);
-                }
-            }
+        if (p.use_tma) {
+            if (threadIdx.x == 0) stage_x_regions_tma<B>(p, xs, bars);
         } else {
-            stage_x_sliced<B>(p, xs, bars, J);
+            stage_x_regions_cp_async<B>(p, xs, bars);
         }
         trace(3);
         int tr_sweep = 4;
-        const uint32_t xlane = xs + (uint32_t)lane * 128u;
-        const int64_t total = myrows * J;  // sweeps of this warp
-        int64_t row = r0 + warp;
-        int j = 0;
-        uint32_t xc = xlane;
-        bool first = true;  // x slices still to be waited for (first row only)
-        auto consume = [&](const uint4& w) {
-            if (first) mbar_wait0(bars + 8 * j);
-            trace(tr_sweep++);
-            if (j < J - 1 || lane < lastw) chunk<B>(acc, w, xc, bstride, off);
-            xc += 4096u;
-            if (++j == J) {
+
+        // consumer state
+        int cu = u0, ch = 0, ck = 0, cJ = 1;
+        bool clast_on = false;
+        uint32_t xc = xs, bstride = 0;
+        uint32_t seen = 0;  // bit h: this warp has completed a part-h unit (its x slices landed)
+        auto c_setup = [&]() {
+            ch = P == 2 ? (cu & 1) : 0;
+            cJ = ch ? p.J1 : p.J0;
+            clast_on = lane < (ch ? plen1 : p.split) - 32 * (cJ - 1);
+            bstride = (uint32_t)cJ * 4096u;
+            xc = xs + (ch ? (uint32_t)(B * p.J0 * 4096) : 0u) + (uint32_t)lane * 128u;
+            ck = 0;
+        };
+        if (cu < u1) c_setup();
+        auto finish_unit = [&]() {
+            const int64_t row = r0 + (P == 2 ? (cu >> 1) : cu);
+            if (P == 1) {
                 reduce_to<B>(acc, sc);
-                epilogue<B>(p, sc, row);
-                trace(tr_sweep++);
-                acc.zero();
-                j = 0;
-                xc = xlane;
-                row += nwarps;
-                first = false;
+                epilogue<B>(p, sc, nullptr, row, srow(row));
+                return;
+            }
+            const bool head = cu == u0 && ch == 1;      // part 0 is the previous warp's
+            const bool tail = cu == u1 - 1 && ch == 0;  // part 1 is the next warp's
+            if (head || tail) {
+                float* sl = reinterpret_cast<float*>(smem + SL.slot_off) +
+                            (head ? warp : warp + 1) * 2 * NV;
+                int* c = reinterpret_cast<int*>(smem + SL.cnt_off) + (head ? warp : warp + 1);
+                reduce_to<B>(acc, sl + ch * NV);
+                int old = 0;
+                if (lane == 0) {
+                    __threadfence_block();
+                    old = atomicAdd(c, 1);
+                }
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old == 1) {  // the other part is in: this warp finishes the row
+                    __threadfence_block();
+                    epilogue<B>(p, sl, sl + NV, row, srow(row));
+                }
+            } else {
+                reduce_to<B>(acc, sc + ch * NV);
+                if (ch == 1) epilogue<B>(p, sc, sc + NV, row, srow(row));
             }
         };
-        // unrolled by two with fixed registers: q0 holds even sweeps, q1 odd sweeps
-        for (int64_t s = 0; s < total; s += 2) {
-            consume(qa);
-            qa = load_next();
-            if (s + 1 < total) {
-                consume(qb);
-                qb = load_next();
+        auto consume = [&](const uint4& w) {
+            if (!((seen >> ch) & 1u)) mbar_wait0(bars + 8 * ((ch ? p.J0 : 0) + ck));
+            trace(tr_sweep++);
+            // lanes past the part's end (last sweep) get all-zero codes: no predicate fires,
+            // and their x reads stay inside the slice -- no divergent branch
+            const bool on = ck < cJ - 1 || clast_on;
+            const uint4 wv = make_uint4(on ? w.x : 0u, on ? w.y : 0u, on ? w.z : 0u, on ? w.w : 0u);
+            if (!(p.dbg & 2)) chunk<B>(acc, wv, xc, bstride, off);
+            xc += 4096u;
+            if (++ck == cJ) {
+                finish_unit();
+                trace(tr_sweep++);
+                acc.zero();
+                seen |= 1u << ch;
+                ++cu;
+                if (cu < u1) c_setup();
+            }
+        };
+#if WW_WEIGHT_RING
+        int slot = 0;
+        uint32_t phase = 0;
+#pragma unroll 1
+        for (int sw = 0; sw < total; ++sw) {
+            mbar_wait(rbar + 8u * (uint32_t)slot, phase);
+            const uint4 w = lds128u(ring + 512u * (uint32_t)slot + 16u * (uint32_t)lane);
+            consume(w);
+            __syncwarp();  // every lane has consumed the slot before it is refilled
+            if (sw + K < total) issue(slot);
+            if (++slot == K) {
+                slot = 0;
+                phase ^= 1u;
             }
         }
+#else
+#pragma unroll 1
+        for (int sw = 0; sw < total; ++sw) {
+            const uint4 cur = qa;
+            qa = qb;
+            qb = load_next();
+            consume(cur);
+        }
+#endif
         return;
     }
 
     // x does not fit one tile: row waves, each streaming the tiles with CTA-wide syncs
+    const int TC = p.tile_chunks;
+    const uint32_t bstride = (uint32_t)p.x_stride * 128u;
     pdl_wait();
     for (int64_t wr = r0; wr < r1; wr += nwarps) {  // uniform across the CTA
         const int64_t row = wr + warp;
@@ -504,7 +694,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             const int64_t c0 = (int64_t)t * TC;
             const int tc_n = (int)(p.W - c0 < TC ? p.W - c0 : TC);
             __syncthreads();  // previous tile fully consumed
-            stage_x<B>(p, xs, c0, 0, tc_n);
+            stage_x<B>(p, xs, c0, tc_n);
             cp_async_wait_all();
             __syncthreads();
             if (active) {
@@ -521,7 +711,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         }
         if (active) {
             reduce_to<B>(acc, sc);
-            epilogue<B>(p, sc, row);
+            epilogue<B>(p, sc, nullptr, row, p.scales + (p.per_row_scales ? 4 * row : 0));
             acc.zero();
         }
     }
@@ -573,30 +763,61 @@ int num_sms() {
     return cached;
 }
 
+// rows of scales a CTA stages in shared memory (0: read from global in the epilogue)
+int scale_rows_for(const ww_layer* L, int64_t grid) {
+    if (L->scale_mode != WW_SCALES_PER_ROW) return 1;
+    const int64_t rows = (L->n + grid - 1) / grid;
+    return rows <= 1024 ? (int)rows : 0;
+}
+
 ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     const int64_t W = ww::words_per_row(L->m);
-    const int64_t per_chunk = (int64_t)B * 128;  // x bytes per chunk for B vectors
-    int64_t tc = kXBudgetBytes / per_chunk;
-    if (tc >= W) {
-        tc = W;
-    } else {
-        tc = std::max<int64_t>(32, tc / 32 * 32);  // whole lane sweeps per tile
-    }
-    const int64_t ntiles = (W + tc - 1) / tc;
-    // one CTA per SM (persistent); a CTA's rows split into equal waves over its warps
+    const int warps = warps_for_b(B);
+    // one CTA per SM (persistent), each owning a contiguous, balanced row range
     const int64_t grid = std::min<int64_t>(sms, L->n);
-    const int max_warps = B <= 4 ? 16 : 8;
-    const int64_t rows_cta = (L->n + grid - 1) / grid;
-    const int64_t waves = (rows_cta + max_warps - 1) / max_warps;
-    const int warps = (int)((rows_cta + waves - 1) / waves);
-    const int64_t xstride = (tc + 31) / 32 * 32;  // whole 32-chunk sweeps per vector
-    const SmemLayout SL = smem_layout(B, (int)xstride, warps, (int)ntiles);
+    const int srows = scale_rows_for(L, grid);
+    // Single x tile: rows of >= 64 chunks are split into two column parts;
+    // the choice depends on (m, B) only.
+    int parts = W >= 64 ? 2 : 1;
+    int64_t split = parts == 2 ? W / 2 : W;
+    int64_t J0 = (split + 31) / 32, J1 = parts == 2 ? (W - split + 31) / 32 : 0;
+    if ((int64_t)B * 32 * (J0 + J1) * 128 > kXBudgetBytes && parts == 2) {
+        parts = 1;
+        split = W;
+        J0 = (W + 31) / 32;
+        J1 = 0;
+    }
     li->grid = (int32_t)grid;
     li->block = 32 * warps;
-    li->tile_chunks = (int32_t)tc;
-    li->tiles = (int32_t)ntiles;
-    li->smem_bytes = (int32_t)SL.total;
     li->num_sms = sms;
+    if ((int64_t)B * 32 * (J0 + J1) * 128 <= kXBudgetBytes) {
+        li->tile_chunks = (int32_t)W;
+        li->tiles = 1;
+        li->parts = parts;
+        li->split_chunks = (int32_t)split;
+        // weight-ring depth: as many 512-B slots per warp as fit next to x while two CTAs
+        // (this layer and the PDL-launched next one) share the SM for B == 1
+        const int nb = (int)(J0 + J1);
+        const int64_t fixed =
+            smem_layout(B, (int)(32 * (J0 + J1)), warps, true, nb, 0, srows).total;
+        const int64_t budget = (B == 1 ? 113 : 226) * 1024;
+        int64_t ring = (budget - fixed) / ((int64_t)warps * (512 + 8));
+        ring = WW_WEIGHT_RING ? std::max<int64_t>(2, std::min<int64_t>(kMaxRing, ring)) : 0;
+        li->ring_slots = (int32_t)ring;
+        li->smem_bytes =
+            (int32_t)smem_layout(B, (int)(32 * (J0 + J1)), warps, true, nb, (int)ring, srows)
+                .total;
+        return WW_OK;
+    }
+    // x does not fit: column tiles of whole 32-chunk sweeps, one part per row
+    int64_t tc = kXBudgetBytes / ((int64_t)B * 128);
+    tc = std::max<int64_t>(32, tc / 32 * 32);
+    li->tile_chunks = (int32_t)tc;
+    li->tiles = (int32_t)((W + tc - 1) / tc);
+    li->parts = 1;
+    li->split_chunks = (int32_t)W;
+    li->ring_slots = 0;
+    li->smem_bytes = (int32_t)smem_layout(B, (int)tc, warps, false, 0, 0, 0).total;
     return WW_OK;
 }
 
@@ -641,6 +862,12 @@ cudaError_t launch_b(const Params& p, const ww_launch_info& li, cudaStream_t s, 
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
+        // always the largest shared-memory carveout: consecutive launches of different shapes
+        // then never force an L1/shared reconfiguration, and the PDL-launched next layer's CTA
+        // can co-reside with this one
+        e = cudaFuncSetAttribute(wl_gemv_kernel<B>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -669,6 +896,7 @@ cudaError_t launch(const Params& p, const ww_launch_info& li, int B, cudaStream_
 }
 
 bool g_force_cp_async = false;  // tests: exercise the per-thread cp.async staging path
+int g_debug_flags = 0;           // tools/chain_time.py: Params::dbg
 
 ww_status check_layer(const ww_layer* L, const char* fn) {
     if (!L) return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: null layer", fn);
@@ -682,7 +910,7 @@ ww_status check_layer(const ww_layer* L, const char* fn) {
         return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: scale_mode %d", fn, L->scale_mode);
     if (L->conv != WW_CONV_EQ1 && L->conv != WW_CONV_ALG1)
         return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: conv %d", fn, L->conv);
-    if (L->n > (int64_t)1 << 40 || L->m > (int64_t)1 << 36)
+    if (L->n > (int64_t)1 << 30 || L->m > (int64_t)1 << 30)
         return ww::fail(WW_ERR_UNSUPPORTED, "%s: shape too large", fn);
     return WW_OK;
 }
@@ -691,6 +919,8 @@ ww_status check_layer(const ww_layer* L, const char* fn) {
 
 // Not part of the ABI (no declaration in ww.h): lets the tests force the cp.async staging path.
 extern "C" void ww_debug_force_cp_async(int on) { g_force_cp_async = on != 0; }
+// Not part of the ABI: overhead-measurement switches for tools/chain_time.py (Params::dbg).
+extern "C" void ww_debug_set_flags(int flags) { g_debug_flags = flags; }
 
 extern "C" ww_status ww_query_launch(const ww_layer* L, int32_t B, ww_launch_info* out) {
     ww_status st = check_layer(L, "ww_query_launch");
@@ -745,10 +975,16 @@ extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
     p.conv = L->conv;
     p.tile_chunks = li.tile_chunks;
     p.ntiles = li.tiles;
-
+    p.parts = li.parts;
+    p.split = li.split_chunks;
+    p.J0 = (li.split_chunks + 31) / 32;
+    p.J1 = li.parts == 2 ? (int32_t)((p.W - li.split_chunks + 31) / 32) : 0;
+    p.ring = li.ring_slots;
+    p.scale_rows = li.tiles == 1 ? scale_rows_for(L, li.grid) : 0;
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
     p.x_stride = (li.tile_chunks + 31) / 32 * 32;
     p.use_tma = li.tiles == 1 && !g_force_cp_async ? (encode_x_map(p, B) ? 1 : 0) : 0;
+    p.dbg = g_debug_flags;
     cudaError_t e = launch(p, li, B, (cudaStream_t)stream, (L->flags & WW_FLAG_PDL) != 0);
     if (e != cudaSuccess)
         return ww::fail(WW_ERR_CUDA, "ww_wl_gemv: launch failed: %s", cudaGetErrorString(e));

@@ -1,11 +1,18 @@
 """Decode linear stack of BASELINE config 4: ``layers`` decoder layers x 7 widely-linear
 projections (q, k, v, o: complex 2048->2048; gate, up: 2048->5504; down: 5504->2048), one
-token (B vectors), output rows sharded over ``world`` GPUs with an all-gather of every
-projection's y (north star).
+token (B vectors), output rows sharded over ``world`` GPUs with an all-gather after every
+launch (north star).
+
+Projections that read the same activation are one launch ("stage"), as a decode step runs
+them: q, k and v share the normed hidden state, gate and up share the post-attention one.
+A stage stacks its projections' rows (independent seeded weights and scales per projection),
+so a layer is four dependent launches -- qkv (6144 x 2048), o (2048 x 2048), gate/up
+(11008 x 2048), down (2048 x 5504) -- each followed by its all-gather.  ``fuse=False``
+gives one stage per projection (seven launches per layer).
 
 Host orchestration only: weights are drawn on the GPU by ``ww_inputs`` and packed by the
-library's device packer; every projection runs in ``ww_wl_gemv`` / ``ww_wl_gemv_batched``
-and every exchange is a NCCL all-gather through ``torch.distributed``.
+library's device packer; every stage runs in ``ww_wl_gemv_batched`` and every exchange is a
+NCCL all-gather through ``torch.distributed``.
 """
 from __future__ import annotations
 
@@ -20,6 +27,11 @@ from . import (CONV_EQ1, FLAG_PDL, LAYOUT_COL4, SCALES_PER_ROW, Layer, packed_by
                pack_ternary_device, shard_plan, wl_gemv_batched)
 
 PROJ_NAMES = ("q", "k", "v", "o", "gate", "up", "down")
+FUSED_STAGES = (("qkv", (0, 1, 2)), ("o", (3,)), ("gateup", (4, 5)), ("down", (6,)))
+UNFUSED_STAGES = tuple((PROJ_NAMES[p], (p,)) for p in range(7))
+# the projection whose seed draws a projection's input x: q, k, v read one activation and
+# gate, up another, fused or not
+X_GROUP = (0, 0, 0, 3, 4, 4, 6)
 
 
 def exchange_shards(y, rank: int, world: int, group=None):
@@ -39,98 +51,129 @@ def gathered_rows(y, world: int, B: int, rows_per_rank: int, n: int, b: int = 0)
 
 
 @dataclass
-class Proj:
-    layer: int
+class Member:
+    """One projection inside a stage: its rows are [row0, row0 + spec.n) of the stage."""
     proj: int
     spec: object          # ww_inputs.LayerSpec
     seed: int             # per-projection seed (ww_inputs.layer_seed)
-    shard: object         # ww.Shard of this rank
-    off: int              # byte offset of the local packed rows in the weight buffer
-    nbytes: int           # local packed bytes
-    soff: int             # float offset of the local scales
-    xoff: int             # complex offset of this projection's input in X
-    ylocal: int           # local rows (may be 0)
+    row0: int
+
+
+@dataclass
+class Stage:
+    layer: int
+    name: str
+    members: list
+    n: int                # stacked rows of the stage
+    m: int
+    shard: object         # ww.Shard of this rank over the stage's n rows
+    off: int = 0          # byte offset of the local packed rows in the weight buffer
+    nbytes: int = 0
+    soff: int = 0         # float offset of the local scales
+    xoff: int = 0         # complex offset of the stage's input in X
+    ylocal: int = 0       # local rows (may be 0)
+    index: int = 0
+    x_seed: int = 0       # seed of the stage's input activation (ww_inputs.activations)
 
     @property
-    def name(self):
-        return f"L{self.layer}.{PROJ_NAMES[self.proj]}"
+    def label(self):
+        return f"L{self.layer}.{self.name}"
 
 
 class WLStack:
-    """All projections of the stack resident in HBM on one rank (its row shard)."""
+    """All stages of the stack resident in HBM on one rank (its row shard of every stage)."""
 
     def __init__(self, layers: int = wi.C4_LAYERS, seed: int = 0, B: int = 1, rank: int = 0,
                  world: int = 1, conv: int = CONV_EQ1, pdl: bool = True, device=None,
-                 group=None):
+                 group=None, fuse: bool = True):
         self.layers, self.seed, self.B, self.rank, self.world = layers, seed, B, rank, world
         self.conv, self.group = conv, group
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.flags = FLAG_PDL if pdl else 0
-        self.projs: list[Proj] = []
+        self.stages: list[Stage] = []
         off = soff = xoff = 0
         for l in range(layers):
-            for p, spec in enumerate(wi.C4_PROJS):
-                sh = shard_plan(spec.n, spec.m, world, rank)
+            for name, projs in (FUSED_STAGES if fuse else UNFUSED_STAGES):
+                members, r0 = [], 0
+                for p in projs:
+                    spec = wi.C4_PROJS[p]
+                    members.append(Member(p, spec, wi.layer_seed(seed, l, p), r0))
+                    r0 += spec.n
+                m = members[0].spec.m
+                sh = shard_plan(r0, m, world, rank)
                 nloc = sh.row_end - sh.row_begin
-                self.projs.append(Proj(l, p, spec, wi.layer_seed(seed, l, p), sh, off,
-                                       nloc * packed_bytes(1, spec.m), soff, xoff, nloc))
-                off += nloc * packed_bytes(1, spec.m)
+                st = Stage(l, name, members, r0, m, sh, off, nloc * packed_bytes(1, m), soff,
+                           xoff, nloc, len(self.stages),
+                           wi.layer_seed(seed, l, X_GROUP[projs[0]]))
+                self.stages.append(st)
+                off += st.nbytes
                 soff += 4 * nloc
-                xoff += B * spec.m
+                xoff += B * m
         self.weight_bytes = off
         self.W = torch.empty(max(off, 16), dtype=torch.uint8, device=self.device)
         self.S = torch.empty(max(soff, 4), dtype=torch.float32, device=self.device)
         self.X = torch.empty(max(xoff, 1), dtype=torch.complex64, device=self.device)
-        # gathered outputs: [world][B][rows_per_rank] per projection (rank-major, ww.h)
-        self.Y = [torch.zeros(p.shard.n_padded * B, dtype=torch.complex64, device=self.device)
-                  for p in self.projs]
+        # gathered outputs: [world][B][rows_per_rank] per stage (rank-major, ww.h)
+        self.Y = [torch.zeros(st.shard.n_padded * B, dtype=torch.complex64, device=self.device)
+                  for st in self.stages]
         self._fill()
 
     # ------------------------------------------------------------------ inputs
     def _fill(self):
         xs_host = np.empty(self.X.numel(), dtype=np.complex64)
-        for pr in self.projs:
-            n, m = pr.spec.n, pr.spec.m
-            if pr.ylocal:
-                planes = torch.empty((4, pr.ylocal, m), dtype=torch.int8, device=self.device)
-                for q in range(4):
-                    wi.codes_device(pr.seed, q, pr.ylocal, m, planes[q], pr.spec.dist,
-                                    row0=pr.shard.row_begin)
-                pack_ternary_device(planes, out=self.W[pr.off:pr.off + pr.nbytes])
-                sc = wi.scales(pr.seed, n, pr.spec.per_row, pr.spec.scale_lo, pr.spec.scale_hi)
-                self.S[pr.soff:pr.soff + 4 * pr.ylocal] = torch.from_numpy(
-                    np.ascontiguousarray(sc[pr.shard.row_begin:pr.shard.row_end]).reshape(-1))
-            xs_host[pr.xoff:pr.xoff + self.B * m] = wi.activations(pr.seed, m, self.B).reshape(-1)
+        for st in self.stages:
+            rb, re = st.shard.row_begin, st.shard.row_end
+            if st.ylocal:
+                planes = torch.empty((4, st.ylocal, st.m), dtype=torch.int8, device=self.device)
+                scales = np.empty((st.ylocal, 4), dtype=np.float32)
+                for mb in st.members:
+                    lo, hi = max(rb, mb.row0), min(re, mb.row0 + mb.spec.n)
+                    if lo >= hi:
+                        continue
+                    for q in range(4):
+                        wi.codes_device(mb.seed, q, hi - lo, st.m, planes[q, lo - rb:hi - rb],
+                                        mb.spec.dist, row0=lo - mb.row0)
+                    sc = wi.scales(mb.seed, mb.spec.n, mb.spec.per_row, mb.spec.scale_lo,
+                                   mb.spec.scale_hi)
+                    scales[lo - rb:hi - rb] = sc[lo - mb.row0:hi - mb.row0]
+                pack_ternary_device(planes, out=self.W[st.off:st.off + st.nbytes])
+                self.S[st.soff:st.soff + 4 * st.ylocal] = torch.from_numpy(scales.reshape(-1))
+            xs_host[st.xoff:st.xoff + self.B * st.m] = wi.activations(st.x_seed, st.m,
+                                                                      self.B).reshape(-1)
         self.X.copy_(torch.from_numpy(xs_host))
         torch.cuda.synchronize(self.device)
 
-    def x_of(self, pr: Proj):
-        return self.X[pr.xoff:pr.xoff + self.B * pr.spec.m].view(self.B, pr.spec.m)
+    def x_of(self, st: Stage):
+        return self.X[st.xoff:st.xoff + self.B * st.m].view(self.B, st.m)
 
-    def y_local_view(self, pr: Proj):
+    def y_local_view(self, st: Stage):
         """This rank's [B][rows_per_rank] slot of the gathered output (first ylocal rows used)."""
-        rpr = pr.shard.rows_per_rank
+        rpr = st.shard.rows_per_rank
         base = self.rank * self.B * rpr
-        return self.Y[self.projs.index(pr)][base:base + self.B * rpr].view(self.B, rpr)
+        return self.Y[st.index][base:base + self.B * rpr].view(self.B, rpr)
 
-    def gathered(self, pr: Proj, b: int = 0):
-        """Full output y[b] (n rows) of a projection after the all-gather."""
-        return gathered_rows(self.Y[self.projs.index(pr)], self.world, self.B,
-                             pr.shard.rows_per_rank, pr.spec.n, b)
+    def gathered(self, st: Stage, b: int = 0):
+        """Full output y[b] (all n rows of the stage) after the all-gather."""
+        return gathered_rows(self.Y[st.index], self.world, self.B, st.shard.rows_per_rank, st.n, b)
+
+    def member_output(self, st: Stage, mb: Member, b: int = 0):
+        """Projection mb's output rows inside the stage's gathered output."""
+        return self.gathered(st, b)[mb.row0:mb.row0 + mb.spec.n]
 
     # ------------------------------------------------------------------ the step
     def launch(self, i: int, stream=None):
-        """Projection i on this rank: WL-GEMV of the local rows into the gathered slot."""
-        pr = self.projs[i]
-        if not pr.ylocal:
+        """Stage i on this rank: WL-GEMV of the local rows into the gathered slot."""
+        st = self.stages[i]
+        if not st.ylocal:
             return 0
-        L = Layer(pr.ylocal, pr.spec.m, LAYOUT_COL4, SCALES_PER_ROW, self.conv, self.flags)
-        wl_gemv_batched(L, self.W[pr.off:pr.off + pr.nbytes], self.S[pr.soff:pr.soff + 4 * pr.ylocal],
-                        self.x_of(pr), self.y_local_view(pr), stream=stream)
+        L = Layer(st.ylocal, st.m, LAYOUT_COL4, SCALES_PER_ROW, self.conv, self.flags)
+        wl_gemv_batched(L, self.W[st.off:st.off + st.nbytes],
+                        self.S[st.soff:st.soff + 4 * st.ylocal], self.x_of(st),
+                        self.y_local_view(st), stream=stream)
         return 1
 
     def exchange(self, i: int):
-        """All-gather of projection i's y shards (NCCL over NVLink); no-op on one rank."""
+        """All-gather of stage i's y shards (NCCL over NVLink); no-op on one rank."""
         if self.world == 1:
             return 0
         exchange_shards(self.Y[i], self.rank, self.world, self.group)
@@ -140,7 +183,7 @@ class WLStack:
         """One token through the whole stack; returns the number of WL-GEMV launches.
         exchange=False skips the all-gathers (tests emulating ranks on one GPU)."""
         k = 0
-        for i in range(len(self.projs)):
+        for i in range(len(self.stages)):
             k += self.launch(i, stream)
             if exchange:
                 self.exchange(i)
@@ -150,15 +193,15 @@ class WLStack:
     def algorithmic_bytes(self) -> int:
         """Bytes the method must move on this rank per step: packed rows + x + y + scales."""
         t = 0
-        for pr in self.projs:
-            if pr.ylocal:
-                t += pr.nbytes + 8 * pr.spec.m * self.B + 8 * pr.ylocal * self.B + 16 * pr.ylocal
+        for st in self.stages:
+            if st.ylocal:
+                t += st.nbytes + 8 * st.m * self.B + 8 * st.ylocal * self.B + 16 * st.ylocal
         return t
 
     def packed_act_bytes(self) -> int:
         """North-star roofline bytes: packed weights + activation (x) bytes on this rank."""
-        return sum(pr.nbytes + 8 * pr.spec.m * self.B for pr in self.projs if pr.ylocal)
+        return sum(st.nbytes + 8 * st.m * self.B for st in self.stages if st.ylocal)
 
     def adds(self) -> int:
         """Algorithmic fp32 add/sub count on this rank (8 per complex column per row, App. D)."""
-        return sum(8 * pr.ylocal * pr.spec.m * self.B for pr in self.projs)
+        return sum(8 * st.ylocal * st.m * self.B for st in self.stages)

@@ -163,3 +163,15 @@ def test_query_launch_shapes():
     assert e.value.status == ww.ERR_UNSUPPORTED
     with pytest.raises(ww.WWError):
         ww.query_launch(ww.Layer(8, 8, layout=ww.LAYOUT_PLANAR), 1)
+
+
+def test_launch_parts_depend_on_m_and_batch_only():
+    for m in (16, 1000, 1024, 2048, 5504):
+        for B in (1, 4, 16):
+            infos = [ww.query_launch(ww.Layer(n, m), B) for n in (1, 148, 2048, 11008)]
+            assert len({(i["parts"], i["split_chunks"]) for i in infos}) == 1
+            W = -(-m // 16)
+            if infos[0]["parts"] == 2:
+                assert infos[0]["split_chunks"] == W // 2 and infos[0]["tiles"] == 1
+            else:
+                assert infos[0]["split_chunks"] == W

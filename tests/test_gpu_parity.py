@@ -107,6 +107,23 @@ def test_determinism_and_pdl_flag():
         assert np.array_equal(y, ys[0])
 
 
+@pytest.mark.parametrize("m", [128, 1000, 2048, 5504])
+def test_row_results_independent_of_n(m):
+    # a row's arithmetic depends on (m, B) only (ww.h ww_launch_info: column parts): the
+    # first n' rows of an n-row layer, launched alone, are bitwise the same for every n'
+    # (different CTA row ranges, different per-warp unit ranges and split-row slots)
+    n = 1500
+    case = LayerCase(n, m, seed=m + 5).device(ww, torch)
+    full = case.gpu(ww, torch, ww.CONV_EQ1)[0]
+    assert_parity(full[None], case.oracle(orc.CONV_EQ1), case)
+    for n2 in (1, 2, 7, 31, 149, 297, 1000):
+        L = ww.Layer(n2, m)
+        y = ww.wl_gemv(L, case.packed_d[:ww.packed_bytes(n2, m)], case.scales_d[:n2],
+                       case.x_d[0])
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), full[:n2]), f"n'={n2}"
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_shard_invariance_emulated(world):
     # each rank's slice run on its own (n_local rows), concatenated == unsharded, bitwise

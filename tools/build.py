@@ -93,6 +93,17 @@ def build_trace():
     return out
 
 
+def build_variant(name, defines):
+    """build/libww_<name>.so: the product sources with extra -D flags (kernel A/B timing via
+    WW_LIB_OVERRIDE in tools only)."""
+    out = os.path.join(ROOT, "build", f"libww_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    srcs = [s for s in product_sources() if s.endswith((".cu", ".cc"))]
+    _run([NVCC] + NVCC_FLAGS + [f"-D{d}" for d in defines] +
+         ["-I", os.path.join(ROOT, "include"), "-shared", "-o", out] + srcs)
+    return out
+
+
 def build_all(force=False):
     build_oracle(force)
     build_inputs(force)
@@ -100,4 +111,8 @@ def build_all(force=False):
 
 
 if __name__ == "__main__":
-    build_all(force="--force" in sys.argv)
+    if "--variant" in sys.argv:  # --variant NAME DEF1 DEF2 ...
+        i = sys.argv.index("--variant")
+        build_variant(sys.argv[i + 1], sys.argv[i + 2:])
+    else:
+        build_all(force="--force" in sys.argv)

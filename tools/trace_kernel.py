@@ -18,6 +18,8 @@ import ww_inputs as wi  # noqa: E402
 _tp = os.path.join(ROOT, "build", "libww_trace.so")
 lib = ctypes.CDLL(_tp if os.path.exists(_tp) else build.build_trace())
 lib.ww_debug_set_trace.argtypes = [ctypes.c_void_p]
+lib.ww_debug_set_flags.argtypes = [ctypes.c_int]
+lib.ww_debug_set_flags(int(os.environ.get("WW_DBG", "0")))  # chain_time.py's debug switches
 lib.ww_wl_gemv_batched.restype = ctypes.c_int
 lib.ww_wl_gemv_batched.argtypes = [ctypes.POINTER(ww._Layer), ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
