@@ -34,12 +34,8 @@ namespace {
 template <int B>
 __host__ __device__ constexpr int warps_for() { return B <= 4 ? 16 : 8; }
 inline int warps_for_b(int B) { return B <= 4 ? 16 : 8; }
-constexpr int kXBudgetBytes = 184 * 1024;  // x tile per CTA (one CTA per SM)
-constexpr int kMaxRing = 8;                // weight-ring slots per warp (512 B each)
-#ifndef WW_WEIGHT_RING
-#define WW_WEIGHT_RING 0  // 1: per-warp TMA bulk rings in shared memory (A/B builds; measured
-                          // ~4% slower than the two-sweep register prefetch)
-#endif
+constexpr int kXBudgetBytes = 184 * 1024;  // x tile per CTA (multi-tile path)
+constexpr int64_t kSmemBudget = 226 * 1024; // single-tile path: all shared memory of a CTA
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
@@ -86,10 +82,15 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(
 #ifdef WW_TRACE
 // per-warp event timestamps (globaltimer ns) for tools/trace_kernel.py; not in the product build
 __device__ unsigned long long* g_trace = nullptr;
-__device__ __forceinline__ void trace(int ev) {
+__device__ __forceinline__ void trace(int ev) {  // events 0..29; 30 = SM id, 31 = exit
     if (g_trace && (threadIdx.x & 31) == 0 && ev < 32) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (ev == 30) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            t = sm;
+        }
         g_trace[((size_t)blockIdx.x * 32 + (threadIdx.x >> 5)) * 32 + ev] = t;
     }
 }
@@ -110,9 +111,7 @@ struct alignas(64) Params {
     int32_t parts;        // single-tile path: column parts per row (1 or 2), see plan()
     int32_t split;        // chunks of part 0 (== W when parts == 1)
     int32_t J0, J1;       // 32-chunk sweeps (= x slices) of part 0 and part 1
-    int32_t ring;         // single-tile path: weight-ring slots (one 512-B sweep each) per warp
-    int32_t scale_rows;   // single-tile path: per-CTA row capacity of the shared scale copy
-                          // (0: the epilogue reads scales from global memory)
+    int32_t rows_cap;     // single-tile path: rows per CTA the shared totals / scales hold
     int32_t dbg;          // tools only (ww_debug_set_flags): 1 = skip griddepcontrol.wait,
                           // 2 = skip the accumulation, 8 = bulk L2 prefetch of the CTA's
                           // weights at kernel start (overhead measurement); 0 in the product
@@ -162,22 +161,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait0(uint32_t bar) { mbar_wait(bar, 0); }
 
-// TMA bulk copy (cp.async.bulk, no tensor map) of `bytes` (multiple of 16) from global
-// memory into shared memory, completing on mbarrier `bar`
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ uint4 lds128u(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(addr));
-    return v;
-}
 
 // cp.async of one 16-byte x granule (columns col, col+1 of vector row `src`), zero-filling
 // columns >= m (R6)
@@ -316,12 +299,12 @@ __device__ __forceinline__ void column(float2 (&pos)[4], float2 (&neg)[4], uint3
 }
 
 // One 16-column chunk of one row (its 16-byte COL4 word w) against the staged x of that
-// chunk: 64 codes x B vectors, 2 predicated FADD2 per code and vector.  xc = smem address of
-// the chunk's x for vector 0 (vector b at xc + b*bstride); off[kk] = swizzled offset of
-// column pair kk ((kk ^ (lane & 7)) * 16: the chunk index's low bits are the lane's).
+// chunk: 64 codes x B vectors, 2 predicated FADD2 per code and vector.  xl = smem address of
+// the chunk's x for vector 0 with the swizzle key in bits 4..6 (chunk base | (chunk & 7) << 4;
+// vector b at + b*bstride): granule kk (columns 2kk, 2kk+1) sits at xl ^ (kk << 4), one LOP3
+// per load (the 128B swizzle of the TMA boxes; 32 lanes on 32 chunks hit 32 banks).
 template <int B>
-__device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xc, uint32_t bstride,
-                                      const uint32_t (&off)[8]) {
+__device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xl, uint32_t bstride) {
     constexpr int S = Acc<B>::S, N = Acc<B>::N;
     const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -329,9 +312,10 @@ __device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xc, u
         const uint32_t word = w4[kk >> 1];
         const uint32_t sh = (kk & 1) * 16;
         const uint32_t bits_a = (word >> sh) & 0xffu, bits_b = (word >> (sh + 8)) & 0xffu;
+        const uint32_t xa = xl ^ ((uint32_t)kk << 4);
 #pragma unroll
         for (int b = 0; b < B; ++b) {  // each decoded code drives all B vectors (a9)
-            const float4 v = lds128(xc + b * bstride + off[kk]);
+            const float4 v = lds128(xa + b * bstride);
             column<N>(acc.a[0][0][b], acc.a[0][N - 1][b], bits_a, make_float2(v.x, v.y));
             column<N>(acc.a[S - 1][0][b], acc.a[S - 1][N - 1][b], bits_b, make_float2(v.z, v.w));
         }
@@ -395,50 +379,49 @@ __device__ __forceinline__ void reduce_to(const Acc<B>& acc, float* dst) {
     __syncwarp();
 }
 
-// Epilogue (a8): lane b < B forms the row totals of vector b (part 0, plus part 1 when the
-// row has two parts: T = T0 + T1 in that order), applies the row's 8 scales once
-// (s = the row's [sUr, sUi, sWr, sWi], staged in shared memory when they fit)
-// and stores y.
+// Epilogue arithmetic (a8): the row's 8 scales applied once to its totals T of vector b
+// (s = [sUr, sUi, sWr, sWi]), EQ1 or ALG1 signs, one complex64 store.
+__device__ __forceinline__ void store_y(const Params& p, const float (&T)[8], const float* s,
+                                        int b, int64_t row) {
+    const float sUr = s[0], sUi = s[1], sWr = s[2], sWi = s[3];
+    const float yre = sUr * T[0] - sUi * T[3] + sWr * T[4] + sWi * T[7];          // Eq. 2
+    const float yim = p.conv == WW_CONV_EQ1
+                          ? sUr * T[1] + sUi * T[2] - sWr * T[5] + sWi * T[6]   // Eq. 1
+                          : sUr * T[1] + sUi * T[2] + sWr * T[5] - sWi * T[6];  // Eq. 3
+    reinterpret_cast<float2*>(p.Y)[b * p.ldy + row] = make_float2(yre, yim);
+}
+
+// Multi-tile epilogue: lane b < B takes vector b's totals from the warp scratch T0.
 template <int B>
-__device__ __forceinline__ void epilogue(const Params& p, const float* T0, const float* T1,
-                                         int64_t row, const float* s) {
+__device__ __forceinline__ void epilogue(const Params& p, const float* T0, int64_t row) {
     const int lane = threadIdx.x & 31;
     if (lane < B) {
         float T[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) T[i] = T1 ? T0[8 * lane + i] + T1[8 * lane + i] : T0[8 * lane + i];
-        const float sUr = s[0], sUi = s[1], sWr = s[2], sWi = s[3];
-        const float yre = sUr * T[0] - sUi * T[3] + sWr * T[4] + sWi * T[7];          // Eq. 2
-        const float yim = p.conv == WW_CONV_EQ1
-                              ? sUr * T[1] + sUi * T[2] - sWr * T[5] + sWi * T[6]   // Eq. 1
-                              : sUr * T[1] + sUi * T[2] + sWr * T[5] - sWi * T[6];  // Eq. 3
-        reinterpret_cast<float2*>(p.Y)[lane * p.ldy + row] = make_float2(yre, yim);
+        for (int i = 0; i < 8; ++i) T[i] = T0[8 * lane + i];
+        store_y(p, T, p.scales + (p.per_row_scales ? 4 * row : 0), lane, row);
     }
     __syncwarp();
 }
 
 // Shared-memory carve-up (bytes), identical on host (plan) and device.
 struct SmemLayout {
-    int64_t x_bytes, scratch_off, slot_off, cnt_off, scale_off, bar_off, rbar_off, ring_off, total;
+    int64_t x_bytes, scratch_off, tot_off, scale_off, bar_off, total;
 };
 // x first (1024-B aligned for the 128B-swizzled TMA boxes), then per-warp reduction scratch
-// (2 parts), then -- single tile only -- the split-row slots and counters, one mbarrier per
-// x slice, one mbarrier per weight-ring slot and the per-warp weight rings (K slots of one
-// 32-chunk sweep = 512 B each).  Single tile: x_chunks = 32*(J0+J1) per vector; multi-tile:
-// the tile width.
+// (multi-tile path), then -- single tile only -- the reduced part totals of every CTA row
+// ([rows][parts][NV] floats), the CTA's row scales and one mbarrier per x slice.  Single
+// tile: x_chunks = 32*(J0+J1) per vector; multi-tile: the tile width.
 __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
-                                                  int nbars, int ring, int scale_rows) {
+                                                  int nbars, int rows, int parts) {
     const int64_t nv = next_pow2(8 * B);
     SmemLayout L;
     L.x_bytes = (int64_t)B * x_chunks * 128;
     L.scratch_off = L.x_bytes;
-    L.slot_off = L.scratch_off + (int64_t)warps * 2 * nv * 4;
-    L.cnt_off = L.slot_off + (single ? (int64_t)(warps + 1) * 2 * nv * 4 : 0);
-    L.scale_off = L.cnt_off + (single ? ((int64_t)(warps + 1) * 4 + 15) / 16 * 16 : 0);
-    L.bar_off = L.scale_off + (single ? 16 * (int64_t)scale_rows : 0);
-    L.rbar_off = L.bar_off + (single ? 8 * (int64_t)nbars : 0);
-    L.ring_off = (L.rbar_off + (single ? 8 * (int64_t)warps * ring : 0) + 127) / 128 * 128;
-    L.total = L.ring_off + (single ? (int64_t)warps * ring * 512 : 0) + 1024;  // + base slack
+    L.tot_off = L.scratch_off + (single ? 0 : (int64_t)warps * nv * 4);
+    L.scale_off = L.tot_off + (single ? (int64_t)rows * parts * nv * 4 : 0);
+    L.bar_off = L.scale_off + (single ? 16 * (int64_t)rows : 0);
+    L.total = L.bar_off + (single ? 8 * (int64_t)nbars : 0) + 1024;  // + base alignment slack
     return L;
 }
 
@@ -460,28 +443,25 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     const bool single = p.ntiles == 1;
     const int nbars = single ? p.J0 + p.J1 : 0;
     const SmemLayout SL = smem_layout(B, single ? 32 * (p.J0 + p.J1) : p.x_stride, nwarps,
-                                      single, nbars, p.ring, p.scale_rows);
-    float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * 2 * NV;
+                                      single, nbars, p.rows_cap, p.parts);
+    float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * NV;
     const uint32_t bars = xs + (uint32_t)SL.bar_off;
 
     // balanced contiguous row range of this CTA (A12 row-parallel decomposition)
     const int64_t r0 = (int64_t)blockIdx.x * p.n / gridDim.x;
     const int64_t r1 = (int64_t)(blockIdx.x + 1) * p.n / gridDim.x;
     if (single) {
-        int* cnt = reinterpret_cast<int*>(smem + SL.cnt_off);
-        for (int i = threadIdx.x; i <= nwarps; i += blockDim.x) cnt[i] = 0;
-        // one mbarrier per thread (an init is a shared-memory atomic: a serial loop over the
-        // ~150 barriers costs microseconds); x-slice barriers first, then the ring barriers,
-        // which sit right after them
-        const int nrb = nwarps * p.ring;
-        for (int j = threadIdx.x; j < nbars + nrb; j += blockDim.x)
-            mbar_init(bars + 8 * j, j < nbars ? (p.use_tma ? 1u : blockDim.x) : 1u);
+        // one mbarrier per thread (an init is a shared-memory atomic; a serial loop by one
+        // thread is measurably slow)
+        for (int j = threadIdx.x; j < nbars; j += blockDim.x)
+            mbar_init(bars + 8 * j, p.use_tma ? 1u : blockDim.x);
         fence_barrier_init();
     }
 
     // PDL: let the next kernel launch now.  (A bulk L2 prefetch of the CTA's weights here
     // measured slower -- it competes with the running layer's stream; tools only: dbg & 8.)
     trace(0);
+    trace(30);
     pdl_launch_dependents();
     if (threadIdx.x == 0 && (p.dbg & 8)) {
         const char* wb = reinterpret_cast<const char*>(p.packed + r0 * p.W);
@@ -492,10 +472,6 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     Acc<B> acc;
     acc.zero();
 
-    uint32_t off[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) off[kk] = (uint32_t)((kk ^ (lane & 7)) << 4);
-
     if (single) {
         // Work units: row r of the CTA is split into P = p.parts column parts
         // (a function of m and B only, so a row's arithmetic never depends on n, the shard
@@ -503,87 +479,54 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         // into contiguous per-warp ranges whose sizes differ by at most one, the longer ones
         // on warps 0..e-1, so the four SM sub-partitions (warp % 4) get equal work.  A part
         // is swept in 32-chunk steps (lane = chunk within the step); the warp reduces each
-        // part to 8B totals and the row total is part 0 + part 1.  A row whose parts land on
-        // two warps (at most one per warp boundary) meets in a shared-memory slot.
+        // part to 8B totals in shared memory, and once every warp is done the CTA-wide
+        // epilogue forms row total = part 0 + part 1 (whichever warps computed them).
         // Unit indices are relative to the CTA (int32: n <= 2^30, check_layer).
         const int P = p.parts;
         const int U = (int)(r1 - r0) * P;
         const int ub = U / nwarps, ue = U - ub * nwarps;
         const int u0 = warp * ub + (warp < ue ? warp : ue);
         const int u1 = u0 + ub + (warp < ue ? 1 : 0);
-        const int plen1 = (int)p.W - p.split;  // chunks of part 1
-        // this warp's sweeps: part-1 units are the odd u when P == 2
-        const int n1 = P == 2 ? (u1 >> 1) - (u0 >> 1) : 0;
-        const int total = (u1 - u0 - n1) * p.J0 + n1 * p.J1;
+        const int len0 = p.split, len1 = (int)p.W - p.split;  // chunks per part
+        const int J0 = p.J0, J1 = p.J1;                        // sweeps per part
+        const bool lastok0 = lane < len0 - 32 * (J0 - 1);      // lane active in last sweep
+        const bool lastok1 = lane < len1 - 32 * (J1 - 1);
+        const int n1 = P == 2 ? (u1 >> 1) - (u0 >> 1) : 0;     // part-1 (odd) units
+        const int total = (u1 - u0 - n1) * J0 + n1 * J1;       // this warp's sweeps
+        const int h0 = P == 2 ? (u0 & 1) : 0;
 
-        // Weight stream (a4): each warp owns a ring of K = p.ring shared-memory slots, one
-        // 32-chunk sweep (512 contiguous bytes of a row) per slot, filled by its lane 0 with
-        // TMA bulk copies (cp.async.bulk, one mbarrier per slot).  The first K sweeps are
-        // requested before griddepcontrol.wait -- weights never depend on the previous kernel
-        // -- so they stream in while the previous layer still computes.
         // the CTA's row scales -> shared memory (cp.async, before griddepcontrol.wait: scales
-        // are weights), so no epilogue waits on a global load
-        const bool staged = p.scale_rows > 0;
-        const float* ssm = reinterpret_cast<const float*>(smem + SL.scale_off);
-        if (staged) {
+        // are weights), read by the epilogue at the end
+        {
             const int ns = p.per_row_scales ? 4 * (int)(r1 - r0) : 4;
             const float* src = p.scales + (p.per_row_scales ? 4 * r0 : 0);
             const uint32_t dst = xs + (uint32_t)SL.scale_off;
             for (int i = threadIdx.x; i < ns; i += blockDim.x) cp_async4(dst + 4u * i, src + i);
             cp_async_wait_all();  // this thread's copies; the __syncthreads below publishes them
         }
-        auto srow = [&](int64_t row) -> const float* {
-            return staged ? ssm + (p.per_row_scales ? 4 * (row - r0) : 0)
-                          : p.scales + (p.per_row_scales ? 4 * row : 0);
-        };
-#if WW_WEIGHT_RING
-        const int K = p.ring;
-        const uint32_t ring = xs + (uint32_t)SL.ring_off + (uint32_t)(warp * K * 512);
-        const uint32_t rbar = xs + (uint32_t)SL.rbar_off + (uint32_t)(warp * K * 8);
-#endif
-        int pu = u0, pk = 0, pJ = 1, plen = 0;  // producer position (unit, sweep)
-        const uint4* pf = p.packed;
-        auto p_setup = [&]() {
-            const int h = P == 2 ? (pu & 1) : 0;
-            const int64_t row = r0 + (P == 2 ? (pu >> 1) : pu);
-            pJ = h ? p.J1 : p.J0;
-            plen = h ? plen1 : p.split;
-            pf = p.packed + row * p.W + (h ? p.split : 0);
-            pk = 0;
-        };
-        if (pu < u1) p_setup();
-#if WW_WEIGHT_RING
-        auto issue = [&](int slot) {  // the producer's next sweep into ring slot `slot`
-            if (lane == 0) {
-                const int nch = plen - 32 * pk < 32 ? plen - 32 * pk : 32;
-                const uint32_t bar = rbar + 8u * (uint32_t)slot;
-                mbar_expect_tx(bar, (uint32_t)nch * 16u);
-                bulk_g2s(ring + 512u * (uint32_t)slot, pf + 32 * pk, (uint32_t)nch * 16u, bar);
-            }
-            if (++pk == pJ) {
-                ++pu;
-                if (pu < u1) p_setup();
-            }
-        };
-        __syncthreads();  // mbarrier inits and slot counters visible
-        {
-            const int pre = total < K ? total : K;
-            for (int j = 0; j < pre; ++j) issue(j);
-        }
-#else
-        // register variant: the next two sweeps in registers (lanes past the end load zeros)
+
+        // Weight stream (a4): this warp's units are one contiguous byte range of the CTA's
+        // rows (row-major COL4, part 0 then part 1 of every row); each lane reads its 16-byte
+        // chunk of a sweep with a streaming 128-bit load, two sweeps ahead, issued before
+        // griddepcontrol.wait (weights never depend on the previous kernel).  Lanes past a
+        // part's end load zeros, so no predicate fires for them.
+        const uint4* pp = p.packed + (r0 + (P == 2 ? (u0 >> 1) : u0)) * p.W + (h0 ? len0 : 0) + lane;
+        int pk = 0, ph = h0, pleft = u1 - u0;
         auto load_next = [&]() -> uint4 {
             uint4 w = make_uint4(0, 0, 0, 0);
-            if (pu < u1 && lane < plen - 32 * pk) w = ldg_stream(pf + 32 * pk + lane);
-            if (++pk == pJ) {
-                ++pu;
-                if (pu < u1) p_setup();
+            const int J = ph ? J1 : J0;
+            if (pleft > 0 && (pk < J - 1 || (ph ? lastok1 : lastok0))) w = ldg_stream(pp);
+            pp += 32;
+            if (++pk == J) {
+                pp += (ph ? len1 : len0) - 32 * J;  // next unit starts right after this part
+                pk = 0;
+                ph ^= P - 1;
+                --pleft;
             }
             return w;
         };
         uint4 qa = load_next(), qb = load_next();
-        __syncthreads();  // mbarrier inits and slot counters visible
-#endif
+        __syncthreads();  // mbarrier inits and staged scales visible
         trace(1);
         if (!(p.dbg & 1)) pdl_wait();
         trace(2);
@@ -595,91 +538,49 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         trace(3);
         int tr_sweep = 4;
 
-        // consumer state
-        int cu = u0, ch = 0, ck = 0, cJ = 1;
-        bool clast_on = false;
-        uint32_t xc = xs, bstride = 0;
+        const uint32_t l7 = (uint32_t)(lane & 7) << 4;  // swizzle key of the lane's chunks
+        const uint32_t xb0 = xs + (uint32_t)lane * 128u, xb1 = xb0 + (uint32_t)(B * J0 * 4096);
+        int ck = 0, ch = h0, cu = u0;
+        uint32_t xc = ch ? xb1 : xb0;
         uint32_t seen = 0;  // bit h: this warp has completed a part-h unit (its x slices landed)
-        auto c_setup = [&]() {
-            ch = P == 2 ? (cu & 1) : 0;
-            cJ = ch ? p.J1 : p.J0;
-            clast_on = lane < (ch ? plen1 : p.split) - 32 * (cJ - 1);
-            bstride = (uint32_t)cJ * 4096u;
-            xc = xs + (ch ? (uint32_t)(B * p.J0 * 4096) : 0u) + (uint32_t)lane * 128u;
-            ck = 0;
-        };
-        if (cu < u1) c_setup();
-        auto finish_unit = [&]() {
-            const int64_t row = r0 + (P == 2 ? (cu >> 1) : cu);
-            if (P == 1) {
-                reduce_to<B>(acc, sc);
-                epilogue<B>(p, sc, nullptr, row, srow(row));
-                return;
-            }
-            const bool head = cu == u0 && ch == 1;      // part 0 is the previous warp's
-            const bool tail = cu == u1 - 1 && ch == 0;  // part 1 is the next warp's
-            if (head || tail) {
-                float* sl = reinterpret_cast<float*>(smem + SL.slot_off) +
-                            (head ? warp : warp + 1) * 2 * NV;
-                int* c = reinterpret_cast<int*>(smem + SL.cnt_off) + (head ? warp : warp + 1);
-                reduce_to<B>(acc, sl + ch * NV);
-                int old = 0;
-                if (lane == 0) {
-                    __threadfence_block();
-                    old = atomicAdd(c, 1);
-                }
-                old = __shfl_sync(0xffffffffu, old, 0);
-                if (old == 1) {  // the other part is in: this warp finishes the row
-                    __threadfence_block();
-                    epilogue<B>(p, sl, sl + NV, row, srow(row));
-                }
-            } else {
-                reduce_to<B>(acc, sc + ch * NV);
-                if (ch == 1) epilogue<B>(p, sc, sc + NV, row, srow(row));
-            }
-        };
-        auto consume = [&](const uint4& w) {
-            if (!((seen >> ch) & 1u)) mbar_wait0(bars + 8 * ((ch ? p.J0 : 0) + ck));
-            trace(tr_sweep++);
-            // lanes past the part's end (last sweep) get all-zero codes: no predicate fires,
-            // and their x reads stay inside the slice -- no divergent branch
-            const bool on = ck < cJ - 1 || clast_on;
-            const uint4 wv = make_uint4(on ? w.x : 0u, on ? w.y : 0u, on ? w.z : 0u, on ? w.w : 0u);
-            if (!(p.dbg & 2)) chunk<B>(acc, wv, xc, bstride, off);
-            xc += 4096u;
-            if (++ck == cJ) {
-                finish_unit();
-                trace(tr_sweep++);
-                acc.zero();
-                seen |= 1u << ch;
-                ++cu;
-                if (cu < u1) c_setup();
-            }
-        };
-#if WW_WEIGHT_RING
-        int slot = 0;
-        uint32_t phase = 0;
-#pragma unroll 1
-        for (int sw = 0; sw < total; ++sw) {
-            mbar_wait(rbar + 8u * (uint32_t)slot, phase);
-            const uint4 w = lds128u(ring + 512u * (uint32_t)slot + 16u * (uint32_t)lane);
-            consume(w);
-            __syncwarp();  // every lane has consumed the slot before it is refilled
-            if (sw + K < total) issue(slot);
-            if (++slot == K) {
-                slot = 0;
-                phase ^= 1u;
-            }
-        }
-#else
+        float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][P][NV]
 #pragma unroll 1
         for (int sw = 0; sw < total; ++sw) {
             const uint4 cur = qa;
             qa = qb;
             qb = load_next();
-            consume(cur);
+            if (!((seen >> ch) & 1u)) mbar_wait0(bars + 8 * ((ch ? J0 : 0) + ck));
+            if (tr_sweep < 30) trace(tr_sweep++);
+            if (!(p.dbg & 2)) chunk<B>(acc, cur, xc | l7, (uint32_t)(ch ? J1 : J0) * 4096u);
+            xc += 4096u;
+            if (++ck == (ch ? J1 : J0)) {
+                // reduce this part over the lanes (a7) into the CTA's totals
+                reduce_to<B>(acc, tot + ((P == 2 ? (cu >> 1) : cu) * P + ch) * NV);
+                if (tr_sweep < 30) trace(tr_sweep++);
+                acc.zero();
+                seen |= 1u << ch;
+                ck = 0;
+                ch ^= P - 1;
+                ++cu;
+                xc = ch ? xb1 : xb0;
+            }
         }
-#endif
+        trace(31);
+        // Epilogue (a8) for all rows of the CTA at once: thread t takes (row, vector) items
+        // t, t + blockDim, ...: row total = part 0 + part 1 (in that order), 8 scale
+        // multiplies, one coalesced complex64 store per item.
+        __syncthreads();
+        const int NR = (int)(r1 - r0);
+        for (int it = threadIdx.x; it < NR * B; it += blockDim.x) {
+            const int b = it / NR, lr = it - b * NR;
+            const float* T0 = tot + (lr * P) * NV + 8 * b;
+            float T[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) T[i] = P == 2 ? T0[i] + T0[NV + i] : T0[i];
+            const float* sr = reinterpret_cast<const float*>(smem + SL.scale_off) +
+                              (p.per_row_scales ? 4 * lr : 0);
+            store_y(p, T, sr, b, r0 + lr);
+        }
         return;
     }
 
@@ -704,14 +605,15 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 for (; tc < tc_n; tc += 32) {
                     const uint4 nxt =
                         tc + 32 < tc_n ? ldg_stream(wrow + tc + 32) : make_uint4(0, 0, 0, 0);
-                    chunk<B>(acc, cur, xs + (uint32_t)tc * 128u, bstride, off);
+                    chunk<B>(acc, cur, (xs + (uint32_t)tc * 128u) | ((uint32_t)(lane & 7) << 4),
+                             bstride);
                     cur = nxt;
                 }
             }
         }
         if (active) {
             reduce_to<B>(acc, sc);
-            epilogue<B>(p, sc, nullptr, row, p.scales + (p.per_row_scales ? 4 * row : 0));
+            epilogue<B>(p, sc, row);
             acc.zero();
         }
     }
@@ -763,50 +665,37 @@ int num_sms() {
     return cached;
 }
 
-// rows of scales a CTA stages in shared memory (0: read from global in the epilogue)
-int scale_rows_for(const ww_layer* L, int64_t grid) {
-    if (L->scale_mode != WW_SCALES_PER_ROW) return 1;
-    const int64_t rows = (L->n + grid - 1) / grid;
-    return rows <= 1024 ? (int)rows : 0;
-}
-
 ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     const int64_t W = ww::words_per_row(L->m);
     const int warps = warps_for_b(B);
     // one CTA per SM (persistent), each owning a contiguous, balanced row range
     const int64_t grid = std::min<int64_t>(sms, L->n);
-    const int srows = scale_rows_for(L, grid);
+    const int64_t rows = (L->n + grid - 1) / grid;  // rows per CTA (at most)
     // Single x tile: rows of >= 64 chunks are split into two column parts;
-    // the choice depends on (m, B) only.
+    // the choice depends on (m, B) only (x must fit kXBudgetBytes).
     int parts = W >= 64 ? 2 : 1;
     int64_t split = parts == 2 ? W / 2 : W;
-    int64_t J0 = (split + 31) / 32, J1 = parts == 2 ? (W - split + 31) / 32 : 0;
-    if ((int64_t)B * 32 * (J0 + J1) * 128 > kXBudgetBytes && parts == 2) {
+    auto sweeps = [&](int pr, int64_t sp) {
+        return (sp + 31) / 32 + (pr == 2 ? (W - sp + 31) / 32 : 0);
+    };
+    if (parts == 2 && (int64_t)B * 32 * sweeps(2, split) * 128 > kXBudgetBytes) {
         parts = 1;
         split = W;
-        J0 = (W + 31) / 32;
-        J1 = 0;
     }
+    auto single_bytes = [&](int pr, int64_t sp) {  // + the CTA's row totals and scales
+        return smem_layout(B, (int)(32 * sweeps(pr, sp)), warps, true, (int)sweeps(pr, sp),
+                           (int)std::min<int64_t>(rows, 1 << 20), pr).total;
+    };
     li->grid = (int32_t)grid;
     li->block = 32 * warps;
     li->num_sms = sms;
-    if ((int64_t)B * 32 * (J0 + J1) * 128 <= kXBudgetBytes) {
+    if ((int64_t)B * 32 * sweeps(parts, split) * 128 <= kXBudgetBytes &&
+        single_bytes(parts, split) <= kSmemBudget) {
         li->tile_chunks = (int32_t)W;
         li->tiles = 1;
         li->parts = parts;
         li->split_chunks = (int32_t)split;
-        // weight-ring depth: as many 512-B slots per warp as fit next to x while two CTAs
-        // (this layer and the PDL-launched next one) share the SM for B == 1
-        const int nb = (int)(J0 + J1);
-        const int64_t fixed =
-            smem_layout(B, (int)(32 * (J0 + J1)), warps, true, nb, 0, srows).total;
-        const int64_t budget = (B == 1 ? 113 : 226) * 1024;
-        int64_t ring = (budget - fixed) / ((int64_t)warps * (512 + 8));
-        ring = WW_WEIGHT_RING ? std::max<int64_t>(2, std::min<int64_t>(kMaxRing, ring)) : 0;
-        li->ring_slots = (int32_t)ring;
-        li->smem_bytes =
-            (int32_t)smem_layout(B, (int)(32 * (J0 + J1)), warps, true, nb, (int)ring, srows)
-                .total;
+        li->smem_bytes = (int32_t)single_bytes(parts, split);
         return WW_OK;
     }
     // x does not fit: column tiles of whole 32-chunk sweeps, one part per row
@@ -816,8 +705,7 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     li->tiles = (int32_t)((W + tc - 1) / tc);
     li->parts = 1;
     li->split_chunks = (int32_t)W;
-    li->ring_slots = 0;
-    li->smem_bytes = (int32_t)smem_layout(B, (int)tc, warps, false, 0, 0, 0).total;
+    li->smem_bytes = (int32_t)smem_layout(B, (int)tc, warps, false, 0, 0, 1).total;
     return WW_OK;
 }
 
@@ -979,8 +867,7 @@ extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
     p.split = li.split_chunks;
     p.J0 = (li.split_chunks + 31) / 32;
     p.J1 = li.parts == 2 ? (int32_t)((p.W - li.split_chunks + 31) / 32) : 0;
-    p.ring = li.ring_slots;
-    p.scale_rows = li.tiles == 1 ? scale_rows_for(L, li.grid) : 0;
+    p.rows_cap = (int32_t)((L->n + li.grid - 1) / li.grid);
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
     p.x_stride = (li.tile_chunks + 31) / 32 * 32;
     p.use_tma = li.tiles == 1 && !g_force_cp_async ? (encode_x_map(p, B) ? 1 : 0) : 0;

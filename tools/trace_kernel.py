@@ -1,6 +1,8 @@
 """Per-warp timeline of one WL-GEMV launch (build/libww_trace.so, -DWW_TRACE): globaltimer
 stamps at kernel entry (0), before/after griddepcontrol.wait (1, 2), after issuing the x
-staging (3), then at the start of every sweep and after every row's epilogue (4, 5, ...)."""
+staging (3), then at the start of every sweep and after every unit's epilogue (4..29), the
+SM id (30) and the warp's exit (31).  Prints event percentiles and the spread of per-CTA
+finish times (by SM id).  Usage: trace_kernel.py [n m ...]; WW_DBG=<flags> as chain_time.py."""
 import ctypes
 import os
 import sys
@@ -25,7 +27,11 @@ lib.ww_wl_gemv_batched.argtypes = [ctypes.POINTER(ww._Layer), ctypes.c_void_p, c
                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                    ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
 
-for (n, m) in [(2048, 5504), (148, 5504), (2048, 2048), (5504, 2048)]:
+shapes = [(2048, 5504), (2048, 2048), (11008, 2048)]
+if len(sys.argv) >= 3:
+    a = [int(v) for v in sys.argv[1:]]
+    shapes = list(zip(a[0::2], a[1::2]))
+for (n, m) in shapes:
     planes = torch.empty((4, n, m), dtype=torch.int8, device="cuda")
     for p in range(4):
         wi.codes_device(1, p, n, m, planes[p])
@@ -47,13 +53,24 @@ for (n, m) in [(2048, 5504), (148, 5504), (2048, 2048), (5504, 2048)]:
     t = tr.cpu().numpy().reshape(148, 32, 32).astype(np.int64)
     valid = t[:, :, 0] > 0
     t0 = t[valid][:, 0].min()
-    rel = np.where(t > 0, t - t0, -1)
     print(f"== n={n} m={m}: warps traced {valid.sum()}")
-    w = rel[valid]
-    for ev in range(0, 18):
-        col = w[:, ev]
-        col = col[col >= 0]
+    for ev in list(range(0, 12)) + [31]:
+        col = t[:, :, ev][valid]
+        col = col[col > 0] - t0
         if col.size:
-            print(f"  ev{ev:2d}: min {col.min()/1e3:7.2f} us  median {np.median(col)/1e3:7.2f}  max {col.max()/1e3:7.2f}")
-    last = np.array([r[r >= 0].max() for r in w])
-    print(f"  last event: median {np.median(last)/1e3:.2f} us, max {last.max()/1e3:.2f} us")
+            print(f"  ev{ev:2d}: min {col.min()/1e3:7.2f} us  median {np.median(col)/1e3:7.2f}  "
+                  f"max {col.max()/1e3:7.2f}")
+    # per-CTA finish (last warp exit) and start, by SM id
+    cta_end = np.array([(t[c, :, 31][valid[c]].max() - t0) / 1e3 for c in range(148)
+                        if valid[c].any()])
+    cta_beg = np.array([(t[c, :, 0][valid[c]].min() - t0) / 1e3 for c in range(148)
+                        if valid[c].any()])
+    smid = np.array([t[c, :, 30][valid[c]][0] for c in range(148) if valid[c].any()])
+    print(f"  CTA finish: min {cta_end.min():.2f} p10 {np.percentile(cta_end, 10):.2f} median "
+          f"{np.median(cta_end):.2f} p90 {np.percentile(cta_end, 90):.2f} max {cta_end.max():.2f} us")
+    dur = cta_end - cta_beg
+    print(f"  CTA duration: min {dur.min():.2f} median {np.median(dur):.2f} max {dur.max():.2f} us")
+    order = np.argsort(smid)
+    buckets = [f"{int(smid[order][i]):3d}-{int(smid[order][min(i + 15, len(order) - 1)]):3d}:"
+               f"{dur[order][i:i + 16].mean():6.2f}" for i in range(0, len(order), 16)]
+    print("  mean CTA duration by SM id (16 SMs per bucket): " + "  ".join(buckets))
