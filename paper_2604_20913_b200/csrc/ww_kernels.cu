@@ -26,6 +26,10 @@
 #include "ww.h"
 #include "ww_internal.h"
 
+#ifndef WW_DEBUG_FLAGS
+#define WW_DEBUG_FLAGS 0  // 1: honour Params::dbg (tools/chain_time.py builds build/libww_dbg.so)
+#endif
+
 namespace {
 
 // warps per CTA: 16 while the B accumulators leave room, 8 (255-register cap) above
@@ -43,6 +47,17 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
+    return v;
+}
+
+// the same load, issued only when `pred` holds (else zeros): one predicated LDG, no branch
+__device__ __forceinline__ uint4 ldg_stream_if(const uint4* p, bool pred) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "l"(p), "r"((int)pred));
     return v;
 }
 
@@ -73,16 +88,21 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" :::);
 }
+#if WW_DEBUG_FLAGS
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+#endif
 
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
 #ifdef WW_TRACE
 // per-warp event timestamps (globaltimer ns) for tools/trace_kernel.py; not in the product build
 __device__ unsigned long long* g_trace = nullptr;
-__device__ __forceinline__ void trace(int ev) {  // events 0..29; 30 = SM id, 31 = exit
+// slot = Params::dbg >> 8: tools/trace_kernel.py --chain gives every launch of a captured
+// chain its own 148*32*32 region of the trace buffer
+__device__ __forceinline__ void trace(int slot, int ev) {  // 0..28 events, 29 sweeps done,
+                                                           // 30 = SM id, 31 = exit
     if (g_trace && (threadIdx.x & 31) == 0 && ev < 32) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -91,11 +111,12 @@ __device__ __forceinline__ void trace(int ev) {  // events 0..29; 30 = SM id, 31
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
             t = sm;
         }
-        g_trace[((size_t)blockIdx.x * 32 + (threadIdx.x >> 5)) * 32 + ev] = t;
+        g_trace[(size_t)slot * 148 * 32 * 32 + ((size_t)blockIdx.x * 32 + (threadIdx.x >> 5)) * 32 +
+                ev] = t;
     }
 }
 #else
-__device__ __forceinline__ void trace(int) {}
+__device__ __forceinline__ void trace(int, int) {}
 #endif
 
 struct alignas(64) Params {
@@ -113,6 +134,7 @@ struct alignas(64) Params {
     int32_t J0, J1;       // 32-chunk sweeps (= x slices) of part 0 and part 1
     int32_t rows_cap;     // single-tile path: rows per CTA the shared totals / scales hold
     int32_t dbg;          // tools only (ww_debug_set_flags): 1 = skip griddepcontrol.wait,
+                          // bits 8..: trace slot (WW_TRACE builds),
                           // 2 = skip the accumulation, 8 = bulk L2 prefetch of the CTA's
                           // weights at kernel start (overhead measurement); 0 in the product
 };
@@ -460,15 +482,18 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
 
     // PDL: let the next kernel launch now.  (A bulk L2 prefetch of the CTA's weights here
     // measured slower -- it competes with the running layer's stream; tools only: dbg & 8.)
-    trace(0);
-    trace(30);
+    const int tslot = p.dbg >> 8;
+    trace(tslot, 0);
+    trace(tslot, 30);
     pdl_launch_dependents();
+#if WW_DEBUG_FLAGS
     if (threadIdx.x == 0 && (p.dbg & 8)) {
         const char* wb = reinterpret_cast<const char*>(p.packed + r0 * p.W);
         const int64_t bytes = (r1 - r0) * p.W * 16;
         for (int64_t off = 0; off < bytes; off += 65536)
             prefetch_l2(wb + off, (uint32_t)(bytes - off < 65536 ? bytes - off : 65536));
     }
+#endif
     Acc<B> acc;
     acc.zero();
 
@@ -487,13 +512,11 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         const int ub = U / nwarps, ue = U - ub * nwarps;
         const int u0 = warp * ub + (warp < ue ? warp : ue);
         const int u1 = u0 + ub + (warp < ue ? 1 : 0);
-        const int len0 = p.split, len1 = (int)p.W - p.split;  // chunks per part
-        const int J0 = p.J0, J1 = p.J1;                        // sweeps per part
-        const bool lastok0 = lane < len0 - 32 * (J0 - 1);      // lane active in last sweep
-        const bool lastok1 = lane < len1 - 32 * (J1 - 1);
-        const int n1 = P == 2 ? (u1 >> 1) - (u0 >> 1) : 0;     // part-1 (odd) units
-        const int total = (u1 - u0 - n1) * J0 + n1 * J1;       // this warp's sweeps
-        const int h0 = P == 2 ? (u0 & 1) : 0;
+        // parts have equal length (plan(): P == 2 only for even W), so unit u of the CTA is
+        // chunks [u*len, (u+1)*len) of the CTA's rows, and each part has J = p.J0 sweeps
+        const int len = p.split;                           // chunks per part
+        const int J = p.J0;                                // sweeps per part
+        const bool lastok = lane < len - 32 * (J - 1);     // lane active in a part's last sweep
 
         // the CTA's row scales -> shared memory (cp.async, before griddepcontrol.wait: scales
         // are weights), read by the epilogue at the end
@@ -506,66 +529,69 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         }
 
         // Weight stream (a4): this warp's units are one contiguous byte range of the CTA's
-        // rows (row-major COL4, part 0 then part 1 of every row); each lane reads its 16-byte
-        // chunk of a sweep with a streaming 128-bit load, two sweeps ahead, issued before
-        // griddepcontrol.wait (weights never depend on the previous kernel).  Lanes past a
-        // part's end load zeros, so no predicate fires for them.
-        const uint4* pp = p.packed + (r0 + (P == 2 ? (u0 >> 1) : u0)) * p.W + (h0 ? len0 : 0) + lane;
-        int pk = 0, ph = h0, pleft = u1 - u0;
+        // rows (row-major COL4); each lane reads its 16-byte chunk of a sweep with a streaming
+        // 128-bit load, two sweeps ahead, issued before griddepcontrol.wait (weights never
+        // depend on the previous kernel).  Lanes past a part's end load zeros, so no predicate
+        // fires for them.
+        const uint4* pp = p.packed + r0 * p.W + (int64_t)u0 * len + lane;
+        int pk = 0, pleft = u1 - u0;
         auto load_next = [&]() -> uint4 {
-            uint4 w = make_uint4(0, 0, 0, 0);
-            const int J = ph ? J1 : J0;
-            if (pleft > 0 && (pk < J - 1 || (ph ? lastok1 : lastok0))) w = ldg_stream(pp);
+            const uint4 w = ldg_stream_if(pp, pleft > 0 && (pk < J - 1 || lastok));
             pp += 32;
             if (++pk == J) {
-                pp += (ph ? len1 : len0) - 32 * J;  // next unit starts right after this part
+                pp += len - 32 * J;  // the next unit starts right after this part
                 pk = 0;
-                ph ^= P - 1;
                 --pleft;
             }
             return w;
         };
         uint4 qa = load_next(), qb = load_next();
         __syncthreads();  // mbarrier inits and staged scales visible
-        trace(1);
-        if (!(p.dbg & 1)) pdl_wait();
-        trace(2);
+        trace(tslot, 1);
+#if WW_DEBUG_FLAGS
+        if (!(p.dbg & 1))
+#endif
+            pdl_wait();
+        trace(tslot, 2);
         if (p.use_tma) {
             if (threadIdx.x == 0) stage_x_regions_tma<B>(p, xs, bars);
         } else {
             stage_x_regions_cp_async<B>(p, xs, bars);
         }
-        trace(3);
+        trace(tslot, 3);
         int tr_sweep = 4;
 
         const uint32_t l7 = (uint32_t)(lane & 7) << 4;  // swizzle key of the lane's chunks
-        const uint32_t xb0 = xs + (uint32_t)lane * 128u, xb1 = xb0 + (uint32_t)(B * J0 * 4096);
-        int ck = 0, ch = h0, cu = u0;
-        uint32_t xc = ch ? xb1 : xb0;
-        uint32_t seen = 0;  // bit h: this warp has completed a part-h unit (its x slices landed)
+        const uint32_t xb0 = xs + (uint32_t)lane * 128u, xb1 = xb0 + (uint32_t)(B * J * 4096);
+        const uint32_t bstride = (uint32_t)J * 4096u;
+        uint32_t seen = 0;  // bit h: the x slices of part h have been waited for
         float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][P][NV]
 #pragma unroll 1
-        for (int sw = 0; sw < total; ++sw) {
-            const uint4 cur = qa;
-            qa = qb;
-            qb = load_next();
-            if (!((seen >> ch) & 1u)) mbar_wait0(bars + 8 * ((ch ? J0 : 0) + ck));
-            if (tr_sweep < 30) trace(tr_sweep++);
-            if (!(p.dbg & 2)) chunk<B>(acc, cur, xc | l7, (uint32_t)(ch ? J1 : J0) * 4096u);
-            xc += 4096u;
-            if (++ck == (ch ? J1 : J0)) {
-                // reduce this part over the lanes (a7) into the CTA's totals
-                reduce_to<B>(acc, tot + ((P == 2 ? (cu >> 1) : cu) * P + ch) * NV);
-                if (tr_sweep < 30) trace(tr_sweep++);
-                acc.zero();
+        for (int u = u0; u < u1; ++u) {
+            const int ch = P == 2 ? (u & 1) : 0;
+            if (!((seen >> ch) & 1u)) {  // first unit of this part: its x slices must be in
+                for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * (ch * J + j));
                 seen |= 1u << ch;
-                ck = 0;
-                ch ^= P - 1;
-                ++cu;
-                xc = ch ? xb1 : xb0;
             }
+            uint32_t xc = (ch ? xb1 : xb0) | l7;
+#pragma unroll 1
+            for (int k = 0; k < J; ++k) {
+                const uint4 cur = qa;
+                qa = qb;
+                qb = load_next();
+                if (tr_sweep < 29) trace(tslot, tr_sweep++);
+#if WW_DEBUG_FLAGS
+                if (!(p.dbg & 2))
+#endif
+                    chunk<B>(acc, cur, xc, bstride);
+                xc += 4096u;
+            }
+            // reduce this part over the lanes (a7) into the CTA's totals
+            reduce_to<B>(acc, tot + u * NV);
+            if (tr_sweep < 29) trace(tslot, tr_sweep++);
+            acc.zero();
         }
-        trace(31);
+        trace(tslot, 29);  // sweeps done
         // Epilogue (a8) for all rows of the CTA at once: thread t takes (row, vector) items
         // t, t + blockDim, ...: row total = part 0 + part 1 (in that order), 8 scale
         // multiplies, one coalesced complex64 store per item.
@@ -581,6 +607,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                               (p.per_row_scales ? 4 * lr : 0);
             store_y(p, T, sr, b, r0 + lr);
         }
+        trace(tslot, 31);
         return;
     }
 
@@ -673,7 +700,7 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     const int64_t rows = (L->n + grid - 1) / grid;  // rows per CTA (at most)
     // Single x tile: rows of >= 64 chunks are split into two column parts;
     // the choice depends on (m, B) only (x must fit kXBudgetBytes).
-    int parts = W >= 64 ? 2 : 1;
+    int parts = W >= 64 && W % 2 == 0 ? 2 : 1;  // two equal parts
     int64_t split = parts == 2 ? W / 2 : W;
     auto sweeps = [&](int pr, int64_t sp) {
         return (sp + 31) / 32 + (pr == 2 ? (W - sp + 31) / 32 : 0);

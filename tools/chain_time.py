@@ -10,7 +10,10 @@ bench contract), split into its parts with the library's debug switches
              reductions and epilogue only
   l2pf       PDL + a bulk L2 prefetch of each CTA's weights at kernel start
 
-Weights rotate over R replicas >= 4x L2 (HBM-cold).  Usage: chain_time.py [n m ...]."""
+Weights rotate over R replicas >= 4x L2 (HBM-cold).  The debug switches need a build with
+-DWW_DEBUG_FLAGS=1: run with WW_LIB_OVERRIDE=build/libww_dbg.so (tools/build.py --variant dbg
+WW_DEBUG_FLAGS=1); with the product library only the pdl / nopdl modes are meaningful.
+Usage: chain_time.py [--product] [n m ...]."""
 import ctypes
 import os
 import sys
@@ -72,14 +75,16 @@ def chain(n, m, B=1, mode="pdl", l2=126 * 2**20, reps=15):
 if __name__ == "__main__":
     print(torch.cuda.get_device_name(), flush=True)
     shapes = [(2048, 2048), (5504, 2048), (2048, 5504), (6144, 2048), (11008, 2048)]
-    if len(sys.argv) >= 3:
-        a = [int(v) for v in sys.argv[1:]]
+    nums = [v for v in sys.argv[1:] if not v.startswith("--")]
+    if len(nums) >= 2:
+        a = [int(v) for v in nums]
         shapes = list(zip(a[0::2], a[1::2]))
-    if "--scan" in sys.argv:
+    if "--scan" in sys.argv:  # noqa: SIM102
         shapes = [(148 * k, m) for m in (2048, 5504) for k in (1, 4, 14, 28, 56)]
     for n, m in shapes:
         codes = 4 * n * m
-        modes = ("pdl", "nopdl", "nowait", "nocompute", "l2pf", "nocompute_l2pf")
+        modes = ("pdl", "nopdl") if "--product" in sys.argv else (
+            "pdl", "nopdl", "nowait", "nocompute", "l2pf", "nocompute_l2pf")
         res = {md: chain(n, m, mode=md) for md in modes}
         rate = codes / (res["pdl"] * 1e-6) / 148 / 1.965e9
         print(f"n={n:6d} m={m:5d}: " + "  ".join(f"{k} {v:6.2f} us" for k, v in res.items())
