@@ -129,9 +129,9 @@ struct alignas(64) Params {
     int32_t per_row_scales, conv, tile_chunks, ntiles, aligned16;
     int32_t x_stride;     // multi-tile path: chunks per vector in the shared x tile
     int32_t use_tma;      // stage x with cp.async.bulk.tensor (else per-thread cp.async)
-    int32_t parts;        // single-tile path: column parts per row (1 or 2), see plan()
-    int32_t split;        // chunks of part 0 (== W when parts == 1)
-    int32_t J0, J1;       // 32-chunk sweeps (= x slices) of part 0 and part 1
+    int32_t parts;        // single-tile path: equal column parts per row (1, 2 or 4), plan()
+    int32_t split;        // chunks per part (W / parts)
+    int32_t J0;           // 32-chunk sweeps (= x slices) per part
     int32_t rows_cap;     // single-tile path: rows per CTA the shared totals / scales hold
     int32_t dbg;          // tools only (ww_debug_set_flags): 1 = skip griddepcontrol.wait,
                           // bits 8..: trace slot (WW_TRACE builds),
@@ -217,53 +217,47 @@ __device__ __forceinline__ void stage_x(const Params& p, uint32_t xs, int64_t c0
     }
 }
 
-// Single-tile x staging.  Part h of the row (chunks [lo_h, lo_h + len_h)) has its own x
-// region at xs + roff_h: vector b's 32*J_h chunks at + b*J_h*4096, chunk c (relative to lo_h)
-// at + c*128, granules swizzled by (c & 7) -- the 128B-swizzle TMA layout, since every
-// region is 1024-B aligned.  Slice j of part h = relative chunks [32j, 32j+32) of every
-// vector, completing mbarrier h*J0 + j.  Slices are issued interleaved (part 0 slice j,
-// part 1 slice j, ...) so the warps that start on part 1 do not wait for all of part 0.
+// Single-tile x staging.  Part h of the row (chunks [h*len, (h+1)*len)) has its own x region
+// at xs + h*B*J*4096: vector b's 32*J chunks at + b*J*4096, chunk c (relative to the part) at
+// + c*128, granules swizzled by (c & 7) -- the 128B-swizzle TMA layout, since every region is
+// 1024-B aligned.  Slice j of part h = relative chunks [32j, 32j+32) of every vector,
+// completing mbarrier h*J + j.
+
 template <int B>
 __device__ __forceinline__ void stage_x_regions_cp_async(const Params& p, uint32_t xs,
                                                          uint32_t bars) {
-    const int jmax = p.J0 > p.J1 ? p.J0 : p.J1;
-    for (int j = 0; j < jmax; ++j) {
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            const int Jh = h ? p.J1 : p.J0, lo = h ? p.split : 0;
-            const uint32_t roff = h ? (uint32_t)(B * p.J0 * 4096) : 0u;
-            if (j >= Jh) continue;
-            const int span = 32 * 8;  // granules per vector in one slice
-            for (int t = threadIdx.x; t < B * span; t += blockDim.x) {
-                const int b = B == 1 ? 0 : t / span;
-                const int g = 32 * 8 * j + (B == 1 ? t : t - b * span);
-                const int tc = g >> 3, gg = g & 7;  // chunk relative to the part
-                const int64_t col = (int64_t)(lo + tc) * 16 + 2 * gg;
-                const uint32_t dst = xs + roff +
-                                     (uint32_t)(((b * Jh * 32 + tc) * 8 + (gg ^ (tc & 7))) * 16);
-                stage_granule(p, dst, p.X + 2 * (b * p.ldx + col), p.m - col);
-            }
-            cp_async_arrive(bars + 8 * (h * p.J0 + j));
+    const int J = p.J0, len = p.split;
+    for (int sl = 0; sl < p.parts * J; ++sl) {
+        const int h = sl / J, j = sl - h * J;
+        const uint32_t roff = (uint32_t)(h * B * J * 4096);
+        const int span = 32 * 8;  // granules per vector in one slice
+        for (int t = threadIdx.x; t < B * span; t += blockDim.x) {
+            const int b = B == 1 ? 0 : t / span;
+            const int g = 32 * 8 * j + (B == 1 ? t : t - b * span);
+            const int tc = g >> 3, gg = g & 7;  // chunk relative to the part
+            const int64_t col = (int64_t)(h * len + tc) * 16 + 2 * gg;
+            const uint32_t dst =
+                xs + roff + (uint32_t)(((b * J * 32 + tc) * 8 + (gg ^ (tc & 7))) * 16);
+            // chunks past the part's end (padding of its last slice) are zero-filled
+            const int64_t valid = tc < len ? p.m - col : 0;
+            stage_granule(p, dst, p.X + 2 * (b * p.ldx + col), valid);
         }
+        cp_async_arrive(bars + 8 * sl);
     }
 }
 
+// one thread per slice issues its TMA boxes (B of them), so all slices are in flight at once
 template <int B>
 __device__ __forceinline__ void stage_x_regions_tma(const Params& p, uint32_t xs, uint32_t bars) {
-    const int jmax = p.J0 > p.J1 ? p.J0 : p.J1;
-    for (int j = 0; j < jmax; ++j) {
+    const int J = p.J0;
+    for (int sl = threadIdx.x; sl < p.parts * J; sl += blockDim.x) {
+        const int h = sl / J, j = sl - h * J;
+        const uint32_t bar = bars + 8 * sl;
+        mbar_expect_tx(bar, (uint32_t)(B * 4096));
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            const int Jh = h ? p.J1 : p.J0, lo = h ? p.split : 0;
-            const uint32_t roff = h ? (uint32_t)(B * p.J0 * 4096) : 0u;
-            if (j >= Jh) continue;
-            const uint32_t bar = bars + 8 * (h * p.J0 + j);
-            mbar_expect_tx(bar, (uint32_t)(B * 4096));
-#pragma unroll 1
-            for (int b = 0; b < B; ++b)
-                tma_load_3d(xs + roff + (uint32_t)((b * Jh + j) * 4096), &p.tmap, 0, lo + 32 * j,
-                            b, bar);
-        }
+        for (int b = 0; b < B; ++b)
+            tma_load_3d(xs + (uint32_t)(h * B * J * 4096 + (b * J + j) * 4096), &p.tmap, 0,
+                        h * p.split + 32 * j, b, bar);
     }
 }
 
@@ -433,7 +427,7 @@ struct SmemLayout {
 // x first (1024-B aligned for the 128B-swizzled TMA boxes), then per-warp reduction scratch
 // (multi-tile path), then -- single tile only -- the reduced part totals of every CTA row
 // ([rows][parts][NV] floats), the CTA's row scales and one mbarrier per x slice.  Single
-// tile: x_chunks = 32*(J0+J1) per vector; multi-tile: the tile width.
+// tile: x_chunks = 32*parts*J per vector; multi-tile: the tile width.
 __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
                                                   int nbars, int rows, int parts) {
     const int64_t nv = next_pow2(8 * B);
@@ -463,8 +457,8 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     const int nwarps = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool single = p.ntiles == 1;
-    const int nbars = single ? p.J0 + p.J1 : 0;
-    const SmemLayout SL = smem_layout(B, single ? 32 * (p.J0 + p.J1) : p.x_stride, nwarps,
+    const int nbars = single ? p.parts * p.J0 : 0;
+    const SmemLayout SL = smem_layout(B, single ? 32 * p.parts * p.J0 : p.x_stride, nwarps,
                                       single, nbars, p.rows_cap, p.parts);
     float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * NV;
     const uint32_t bars = xs + (uint32_t)SL.bar_off;
@@ -512,8 +506,8 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         const int ub = U / nwarps, ue = U - ub * nwarps;
         const int u0 = warp * ub + (warp < ue ? warp : ue);
         const int u1 = u0 + ub + (warp < ue ? 1 : 0);
-        // parts have equal length (plan(): P == 2 only for even W), so unit u of the CTA is
-        // chunks [u*len, (u+1)*len) of the CTA's rows, and each part has J = p.J0 sweeps
+        // parts have equal length (plan(): P divides W), so unit u of the CTA is chunks
+        // [u*len, (u+1)*len) of the CTA's rows, and each part has J = p.J0 sweeps
         const int len = p.split;                           // chunks per part
         const int J = p.J0;                                // sweeps per part
         const bool lastok = lane < len - 32 * (J - 1);     // lane active in a part's last sweep
@@ -554,7 +548,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             pdl_wait();
         trace(tslot, 2);
         if (p.use_tma) {
-            if (threadIdx.x == 0) stage_x_regions_tma<B>(p, xs, bars);
+            stage_x_regions_tma<B>(p, xs, bars);
         } else {
             stage_x_regions_cp_async<B>(p, xs, bars);
         }
@@ -562,18 +556,18 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         int tr_sweep = 4;
 
         const uint32_t l7 = (uint32_t)(lane & 7) << 4;  // swizzle key of the lane's chunks
-        const uint32_t xb0 = xs + (uint32_t)lane * 128u, xb1 = xb0 + (uint32_t)(B * J * 4096);
+        const uint32_t xb0 = xs + (uint32_t)lane * 128u, xpart = (uint32_t)(B * J * 4096);
         const uint32_t bstride = (uint32_t)J * 4096u;
         uint32_t seen = 0;  // bit h: the x slices of part h have been waited for
         float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][P][NV]
 #pragma unroll 1
         for (int u = u0; u < u1; ++u) {
-            const int ch = P == 2 ? (u & 1) : 0;
+            const int ch = u & (P - 1);  // part (P is a power of two)
             if (!((seen >> ch) & 1u)) {  // first unit of this part: its x slices must be in
                 for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * (ch * J + j));
                 seen |= 1u << ch;
             }
-            uint32_t xc = (ch ? xb1 : xb0) | l7;
+            uint32_t xc = (xb0 + (uint32_t)ch * xpart) | l7;
 #pragma unroll 1
             for (int k = 0; k < J; ++k) {
                 const uint4 cur = qa;
@@ -593,8 +587,8 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         }
         trace(tslot, 29);  // sweeps done
         // Epilogue (a8) for all rows of the CTA at once: thread t takes (row, vector) items
-        // t, t + blockDim, ...: row total = part 0 + part 1 (in that order), 8 scale
-        // multiplies, one coalesced complex64 store per item.
+        // t, t + blockDim, ...: row total = ((part 0 + part 1) + part 2) + part 3 (in that
+        // order), 8 scale multiplies, one coalesced complex64 store per item.
         __syncthreads();
         const int NR = (int)(r1 - r0);
         for (int it = threadIdx.x; it < NR * B; it += blockDim.x) {
@@ -602,7 +596,10 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             const float* T0 = tot + (lr * P) * NV + 8 * b;
             float T[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) T[i] = P == 2 ? T0[i] + T0[NV + i] : T0[i];
+            for (int i = 0; i < 8; ++i) T[i] = T0[i];
+            for (int h = 1; h < P; ++h)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) T[i] += T0[h * NV + i];
             const float* sr = reinterpret_cast<const float*>(smem + SL.scale_off) +
                               (p.per_row_scales ? 4 * lr : 0);
             store_y(p, T, sr, b, r0 + lr);
@@ -698,17 +695,19 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     // one CTA per SM (persistent), each owning a contiguous, balanced row range
     const int64_t grid = std::min<int64_t>(sms, L->n);
     const int64_t rows = (L->n + grid - 1) / grid;  // rows per CTA (at most)
-    // Single x tile: rows of >= 64 chunks are split into two column parts;
-    // the choice depends on (m, B) only (x must fit kXBudgetBytes).
-    int parts = W >= 64 && W % 2 == 0 ? 2 : 1;  // two equal parts
-    int64_t split = parts == 2 ? W / 2 : W;
-    auto sweeps = [&](int pr, int64_t sp) {
-        return (sp + 31) / 32 + (pr == 2 ? (W - sp + 31) / 32 : 0);
-    };
-    if (parts == 2 && (int64_t)B * 32 * sweeps(2, split) * 128 > kXBudgetBytes) {
-        parts = 1;
-        split = W;
-    }
+    // Single x tile: a row is split into P = 2 equal column parts of >= 64 chunks (2 sweeps)
+    // when W is even, else P = 1; the choice depends on (m, B) only (x must
+    // fit kXBudgetBytes).  (P = 4 for m = 5504 measured slower: the extra part reductions
+    // cost more than the finer balance gains; the kernel supports any power of two.)
+    int parts = 1;
+    for (int cand : {2})
+        if (W % cand == 0 && W / cand >= 64 &&
+            (int64_t)B * 32 * cand * ((W / cand + 31) / 32) * 128 <= kXBudgetBytes) {
+            parts = cand;
+            break;
+        }
+    const int64_t split = W / parts;
+    auto sweeps = [&](int pr, int64_t sp) { return pr * ((sp + 31) / 32); };
     auto single_bytes = [&](int pr, int64_t sp) {  // + the CTA's row totals and scales
         return smem_layout(B, (int)(32 * sweeps(pr, sp)), warps, true, (int)sweeps(pr, sp),
                            (int)std::min<int64_t>(rows, 1 << 20), pr).total;
@@ -893,7 +892,6 @@ extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
     p.parts = li.parts;
     p.split = li.split_chunks;
     p.J0 = (li.split_chunks + 31) / 32;
-    p.J1 = li.parts == 2 ? (int32_t)((p.W - li.split_chunks + 31) / 32) : 0;
     p.rows_cap = (int32_t)((L->n + li.grid - 1) / li.grid);
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
     p.x_stride = (li.tile_chunks + 31) / 32 * 32;

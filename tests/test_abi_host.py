@@ -166,12 +166,12 @@ def test_query_launch_shapes():
 
 
 def test_launch_parts_depend_on_m_and_batch_only():
-    for m in (16, 1000, 1024, 2048, 5504):
+    for m in (16, 1000, 1024, 2048, 4096, 5504):
         for B in (1, 4, 16):
             infos = [ww.query_launch(ww.Layer(n, m), B) for n in (1, 148, 2048, 11008)]
             assert len({(i["parts"], i["split_chunks"]) for i in infos}) == 1
             W = -(-m // 16)
-            if infos[0]["parts"] == 2:
-                assert infos[0]["split_chunks"] == W // 2 and infos[0]["tiles"] == 1
-            else:
-                assert infos[0]["split_chunks"] == W
+            P = infos[0]["parts"]
+            assert P in (1, 2, 4) and infos[0]["split_chunks"] * P == W
+            if P > 1:
+                assert infos[0]["tiles"] == 1 and W // P >= 64

@@ -107,7 +107,7 @@ def test_determinism_and_pdl_flag():
         assert np.array_equal(y, ys[0])
 
 
-@pytest.mark.parametrize("m", [128, 1000, 2048, 5504])
+@pytest.mark.parametrize("m", [128, 1000, 2048, 4096, 5504])
 def test_row_results_independent_of_n(m):
     # a row's arithmetic depends on (m, B) only (ww.h ww_launch_info: column parts): the
     # first n' rows of an n-row layer, launched alone, are bitwise the same for every n'
