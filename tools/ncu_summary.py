@@ -40,7 +40,9 @@ def main(rep, out_json=None):
             return float(v.replace(",", "")) * mult
         per = [to_bytes(e["dram__bytes_read.sum"]) + to_bytes(e["dram__bytes_write.sum"])
                for e in res if "wl_gemv" in e["kernel"]]
-        json.dump({"source": rep, "dram_bytes_per_launch": per[0] if per else None,
+        # mean over the captured launches (one decoder layer: qkv, o, gate/up, down), the
+        # same averaging as bench.py's per-launch roofline
+        json.dump({"source": rep, "dram_bytes_per_launch": sum(per) / len(per) if per else None,
                    "per_launch": per, "kernels": res}, open(out_json, "w"), indent=1)
 
 
