@@ -26,6 +26,8 @@ import paper_2604_20913_b200 as ww  # noqa: E402
 import ww_inputs as wi  # noqa: E402
 
 ww._lib.ww_debug_set_flags.argtypes = [ctypes.c_int]
+if os.environ.get("WW_FORCE_CP_ASYNC"):  # stage x with per-thread cp.async instead of TMA
+    ww._lib.ww_debug_force_cp_async(1)
 
 
 def chain(n, m, B=1, mode="pdl", l2=126 * 2**20, reps=15):
