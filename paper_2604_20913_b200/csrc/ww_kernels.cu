@@ -811,6 +811,7 @@ cudaError_t launch(const Params& p, const ww_launch_info& li, int B, cudaStream_
 
 bool g_force_cp_async = false;  // tests: exercise the per-thread cp.async staging path
 int g_debug_flags = 0;           // tools/chain_time.py: Params::dbg
+int g_last_use_tma = -1;         // tests: whether the last launch staged x with TMA
 
 ww_status check_layer(const ww_layer* L, const char* fn) {
     if (!L) return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: null layer", fn);
@@ -835,6 +836,8 @@ ww_status check_layer(const ww_layer* L, const char* fn) {
 extern "C" void ww_debug_force_cp_async(int on) { g_force_cp_async = on != 0; }
 // Not part of the ABI: overhead-measurement switches for tools/chain_time.py (Params::dbg).
 extern "C" void ww_debug_set_flags(int flags) { g_debug_flags = flags; }
+// Not part of the ABI: 1 if the last WL-GEMV launch staged x with TMA, 0 cp.async, -1 none yet.
+extern "C" int ww_debug_last_use_tma(void) { return g_last_use_tma; }
 
 extern "C" ww_status ww_query_launch(const ww_layer* L, int32_t B, ww_launch_info* out) {
     ww_status st = check_layer(L, "ww_query_launch");
@@ -897,6 +900,7 @@ extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
     p.x_stride = (li.tile_chunks + 31) / 32 * 32;
     p.use_tma = li.tiles == 1 && !g_force_cp_async ? (encode_x_map(p, B) ? 1 : 0) : 0;
     p.dbg = g_debug_flags;
+    g_last_use_tma = p.use_tma;
     cudaError_t e = launch(p, li, B, (cudaStream_t)stream, (L->flags & WW_FLAG_PDL) != 0);
     if (e != cudaSuccess)
         return ww::fail(WW_ERR_CUDA, "ww_wl_gemv: launch failed: %s", cudaGetErrorString(e));

@@ -216,6 +216,16 @@ def test_argument_errors_before_launch():
     assert e.value.status == ww.ERR_INVALID_ARGUMENT
 
 
+def test_aligned_inputs_take_the_tma_path():
+    # the product staging path: x boxes by cp.async.bulk.tensor (128B swizzle)
+    case = LayerCase.from_spec(wi.C3B, seed=3).device(ww, torch)
+    case.gpu(ww, torch, ww.CONV_EQ1)
+    assert ww._lib.ww_debug_last_use_tma() == 1
+    case = LayerCase(100, 77, seed=8).device(ww, torch)  # 16 does not divide m: cp.async
+    case.gpu(ww, torch, ww.CONV_EQ1)
+    assert ww._lib.ww_debug_last_use_tma() == 0
+
+
 @pytest.mark.parametrize("n,m,B", [(2048, 2048, 1), (300, 5504, 3), (77, 1000, 1)])
 def test_cp_async_staging_path_matches_tma_path(n, m, B):
     # x staged by per-thread cp.async (fallback for 16 !| m, misaligned x, odd ldx) must give
