@@ -144,6 +144,22 @@ typedef struct {
 } ww_launch_info;
 ww_status ww_query_launch(const ww_layer* L, int32_t B, ww_launch_info* out);
 
+/* Unfused ablation (not the product path): the paper's unfused baseline
+ * -- eight real ternary GEMVs per widely-linear layer, one per
+ * (plane, component of x), each re-streaming its plane, then one combine.
+ * ww_ternary_gemv_plane: acc_d[i] = sum_j t_ij * x_j.comp for plane `plane` (0..3 = U_re,
+ * U_im, W_re, W_im) of a WW_LAYOUT_PLANAR buffer (4-B aligned) and component `comp` (0 = re,
+ * 1 = im) of the complex64 vector x_d; acc_d: n fp32.  flags: WW_FLAG_PDL.
+ * ww_wl_combine: y (complex64, n) from acc8_d = 8 x n fp32 partial sums ordered
+ * [U_re.re, U_re.im, U_im.re, U_im.im, W_re.re, W_re.im, W_im.re, W_im.im], the layer's
+ * scales and convention, scales applied once per row.  Both asynchronous on
+ * `stream`; argument errors before any launch. */
+ww_status ww_ternary_gemv_plane(int64_t n, int64_t m, const void* planar_d, int32_t plane,
+                                const float* x_d, int32_t comp, float* acc_d, uint32_t flags,
+                                void* stream);
+ww_status ww_wl_combine(const ww_layer* L, const float* acc8_d, const float* scales_d, float* y_d,
+                        void* stream);
+
 const char* ww_status_string(ww_status s);
 const char* ww_last_error(void); /* thread-local message of the last failing call */
 int32_t ww_version(void);

@@ -36,7 +36,8 @@ MAX_BATCH = 16
 # every symbol include/ww.h declares (tests check the library exports them all)
 EXPORTS = ("ww_packed_bytes", "ww_pack_ternary", "ww_unpack_ternary", "ww_repack",
            "ww_pack_ternary_device", "ww_wl_gemv", "ww_wl_gemv_batched", "ww_shard_plan",
-           "ww_query_launch", "ww_status_string", "ww_last_error", "ww_version")
+           "ww_query_launch", "ww_status_string", "ww_last_error", "ww_version",
+           "ww_ternary_gemv_plane", "ww_wl_combine")
 
 
 class WWError(RuntimeError):
@@ -83,6 +84,10 @@ _lib.ww_shard_plan.restype = _i32
 _lib.ww_shard_plan.argtypes = [_i64, _i64, _i32, _i32, ctypes.POINTER(_Shard)]
 _lib.ww_query_launch.restype = _i32
 _lib.ww_query_launch.argtypes = [ctypes.POINTER(_Layer), _i32, ctypes.POINTER(_LaunchInfo)]
+_lib.ww_ternary_gemv_plane.restype = _i32
+_lib.ww_ternary_gemv_plane.argtypes = [_i64, _i64, _vp, _i32, _vp, _i32, _vp, ctypes.c_uint32, _vp]
+_lib.ww_wl_combine.restype = _i32
+_lib.ww_wl_combine.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _vp]
 _lib.ww_status_string.restype = ctypes.c_char_p
 _lib.ww_status_string.argtypes = [_i32]
 _lib.ww_last_error.restype = ctypes.c_char_p
@@ -227,3 +232,24 @@ def query_launch(layer: Layer, B: int = 1) -> dict:
     L = layer.c()
     _check(_lib.ww_query_launch(ctypes.byref(L), B, ctypes.byref(li)))
     return {f: getattr(li, f) for f, _ in _LaunchInfo._fields_}
+
+
+# --------------------------------------------------------------------------- unfused ablation
+def wl_gemv_unfused(layer: Layer, planar, scales, x, y=None, acc=None, stream=None):
+    """The paper's unfused baseline on the GPU: eight real ternary GEMVs
+    (ww_ternary_gemv_plane: planes U_re, U_im, W_re, W_im of a WW_LAYOUT_PLANAR buffer
+    against x.re and x.im) plus ww_wl_combine.  Ablation only; the product is wl_gemv."""
+    import torch
+    n, m = layer.n, layer.m
+    if y is None:
+        y = torch.empty(n, dtype=torch.complex64, device=x.device)
+    if acc is None:
+        acc = torch.empty((8, n), dtype=torch.float32, device=x.device)
+    s = _stream_ptr(stream)
+    for plane in range(4):
+        for comp in range(2):
+            _check(_lib.ww_ternary_gemv_plane(n, m, planar.data_ptr(), plane, x.data_ptr(), comp,
+                                              acc[2 * plane + comp].data_ptr(), layer.flags, s))
+    L = layer.c()
+    _check(_lib.ww_wl_combine(ctypes.byref(L), acc.data_ptr(), scales.data_ptr(), y.data_ptr(), s))
+    return y

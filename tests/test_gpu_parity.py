@@ -239,3 +239,15 @@ def test_cp_async_staging_path_matches_tma_path(n, m, B):
         ww._lib.ww_debug_force_cp_async(0)
     assert np.array_equal(y_tma, y_cpa)
     assert_parity(y_cpa, case.oracle(orc.CONV_EQ1), case)
+
+
+@pytest.mark.parametrize("n,m", [(2048, 2048), (2048, 5504), (300, 517), (1, 16)])
+@pytest.mark.parametrize("conv", CONVS)
+def test_unfused_ablation_matches_oracle(n, m, conv):
+    # the paper's unfused baseline (8 real ternary GEMVs + combine), NEXT-2 ablation
+    case = LayerCase(n, m, seed=n + 3 * m).device(ww, torch)
+    planar = torch.from_numpy(ww.pack_ternary(case.planes, ww.LAYOUT_PLANAR).view(np.uint8)).cuda()
+    L = ww.Layer(n, m, ww.LAYOUT_PLANAR, ww.SCALES_PER_ROW, conv)
+    y = ww.wl_gemv_unfused(L, planar, case.scales_d, case.x_d[0])
+    torch.cuda.synchronize()
+    assert_parity(y.cpu().numpy()[None], case.oracle(ORC[conv]), case)
