@@ -283,6 +283,19 @@ struct Acc {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) a[s][k][b][q] = make_float2(0.f, 0.f);
     }
+    // the lane's raw accumulators to / from shared memory (hand-off of a split row's state):
+    // float j of lane l at base + (j*32 + l), so a warp's accesses are conflict-free
+    static constexpr int kFloats = S * N * B * 8;
+    __device__ __forceinline__ void store(float* base, int lane) const {
+        const float* f = reinterpret_cast<const float*>(a);
+#pragma unroll
+        for (int j = 0; j < kFloats; ++j) base[j * 32 + lane] = f[j];
+    }
+    __device__ __forceinline__ void load(const float* base, int lane) {
+        float* f = reinterpret_cast<float*>(a);
+#pragma unroll
+        for (int j = 0; j < kFloats; ++j) f[j] = base[j * 32 + lane];
+    }
     // sum over sets of plane q, vector b (pos - neg when N == 2)
     __device__ __forceinline__ float2 total(int b, int q) const {
         float2 t = a[0][0][b][q];
@@ -422,21 +435,25 @@ __device__ __forceinline__ void epilogue(const Params& p, const float* T0, int64
 
 // Shared-memory carve-up (bytes), identical on host (plan) and device.
 struct SmemLayout {
-    int64_t x_bytes, scratch_off, tot_off, scale_off, bar_off, total;
+    int64_t x_bytes, scratch_off, tot_off, scale_off, slot_off, cnt_off, bar_off, total;
 };
 // x first (1024-B aligned for the 128B-swizzled TMA boxes), then per-warp reduction scratch
-// (multi-tile path), then -- single tile only -- the reduced part totals of every CTA row
-// ([rows][parts][NV] floats), the CTA's row scales and one mbarrier per x slice.  Single
-// tile: x_chunks = 32*parts*J per vector; multi-tile: the tile width.
+// (multi-tile path), then -- single tile only -- the reduced totals of every CTA row
+// ([rows][NV] floats), the CTA's row scales, the split-row hand-off slots (one per warp,
+// 32 lanes x the lane's accumulator floats) and their flags, and one mbarrier per x slice.
+// Single tile: x_chunks = 32*parts*J per vector; multi-tile: the tile width.
 __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
                                                   int nbars, int rows, int parts) {
     const int64_t nv = next_pow2(8 * B);
+    const int64_t acc_floats = (B <= 2 ? 2 : 1) * B * 8;  // Acc<B>::kFloats
     SmemLayout L;
     L.x_bytes = (int64_t)B * x_chunks * 128;
     L.scratch_off = L.x_bytes;
     L.tot_off = L.scratch_off + (single ? 0 : (int64_t)warps * nv * 4);
-    L.scale_off = L.tot_off + (single ? (int64_t)rows * parts * nv * 4 : 0);
-    L.bar_off = L.scale_off + (single ? 16 * (int64_t)rows : 0);
+    L.scale_off = L.tot_off + (single ? (int64_t)rows * nv * 4 : 0);
+    L.slot_off = L.scale_off + (single ? 16 * (int64_t)rows : 0);
+    L.cnt_off = L.slot_off + (single && parts > 1 ? (int64_t)(warps + 1) * 32 * acc_floats * 4 : 0);
+    L.bar_off = L.cnt_off + (single ? ((int64_t)(warps + 1) * 4 + 7) / 8 * 8 : 0);
     L.total = L.bar_off + (single ? 8 * (int64_t)nbars : 0) + 1024;  // + base alignment slack
     return L;
 }
@@ -492,25 +509,29 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     acc.zero();
 
     if (single) {
-        // Work units: row r of the CTA is split into P = p.parts column parts
-        // (a function of m and B only, so a row's arithmetic never depends on n, the shard
-        // or the launch shape); unit u = (row u/P, part u%P).  The CTA's NR*P units are cut
-        // into contiguous per-warp ranges whose sizes differ by at most one, the longer ones
-        // on warps 0..e-1, so the four SM sub-partitions (warp % 4) get equal work.  A part
-        // is swept in 32-chunk steps (lane = chunk within the step); the warp reduces each
-        // part to 8B totals in shared memory, and once every warp is done the CTA-wide
-        // epilogue forms row total = part 0 + part 1 (whichever warps computed them).
+        // Work units: row r of the CTA is split into P = p.parts (1 or 2)
+        // column parts (a function of m and B only); unit u = (row u/P, part u%P).  The
+        // CTA's NR*P units are cut into contiguous per-warp ranges whose sizes differ by at
+        // most one, the longer ones on warps 0..e-1, so the four SM sub-partitions (warp % 4)
+        // get equal work.  A row's lane accumulators run over part P-1 first, then part 0
+        // (whichever warps hold them), and the row is reduced once, after part 0: a row split
+        // at a warp boundary has its part 1 at the *start* of the next warp's range, which
+        // hands its lane state to this warp through shared memory before this warp reaches
+        // the row's part 0 at the *end* of its own range.  So a row's arithmetic depends on
+        // (m, B) only -- never on n, the shard, the grid or the warp split.
         // Unit indices are relative to the CTA (int32: n <= 2^30, check_layer).
         const int P = p.parts;
         const int U = (int)(r1 - r0) * P;
         const int ub = U / nwarps, ue = U - ub * nwarps;
         const int u0 = warp * ub + (warp < ue ? warp : ue);
         const int u1 = u0 + ub + (warp < ue ? 1 : 0);
-        // parts have equal length (plan(): P divides W), so unit u of the CTA is chunks
-        // [u*len, (u+1)*len) of the CTA's rows, and each part has J = p.J0 sweeps
         const int len = p.split;                           // chunks per part
         const int J = p.J0;                                // sweeps per part
         const bool lastok = lane < len - 32 * (J - 1);     // lane active in a part's last sweep
+        // rows touched by this warp: [ra, rz]; with P == 2 the first may lack part 0 (its
+        // part 0 is the previous warp's) and the last may lack part 1 (the next warp's)
+        const int ra = u0 / P, rz = (u1 - 1) / P;
+        auto has_part = [&](int r, int h) { return r * P + h >= u0 && r * P + h < u1; };
 
         // the CTA's row scales -> shared memory (cp.async, before griddepcontrol.wait: scales
         // are weights), read by the epilogue at the end
@@ -522,25 +543,33 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             cp_async_wait_all();  // this thread's copies; the __syncthreads below publishes them
         }
 
-        // Weight stream (a4): this warp's units are one contiguous byte range of the CTA's
-        // rows (row-major COL4); each lane reads its 16-byte chunk of a sweep with a streaming
-        // 128-bit load, two sweeps ahead, issued before griddepcontrol.wait (weights never
+        // Weight stream (a4): the warp's units in processing order (per row: part P-1, then
+        // part 0); each lane reads its 16-byte chunk of a sweep with a streaming 128-bit load,
+        // two sweeps ahead, the first two issued before griddepcontrol.wait (weights never
         // depend on the previous kernel).  Lanes past a part's end load zeros, so no predicate
         // fires for them.
-        const uint4* pp = p.packed + r0 * p.W + (int64_t)u0 * len + lane;
-        int pk = 0, pleft = u1 - u0;
+        int pr = ra, ph = has_part(ra, P - 1) ? P - 1 : 0, pk = 0;
         auto load_next = [&]() -> uint4 {
-            const uint4 w = ldg_stream_if(pp, pleft > 0 && (pk < J - 1 || lastok));
-            pp += 32;
+            const uint4* q = p.packed + (r0 + pr) * p.W + ph * len + 32 * pk + lane;
+            const uint4 w = ldg_stream_if(q, pr <= rz && (pk < J - 1 || lastok));
             if (++pk == J) {
-                pp += len - 32 * J;  // the next unit starts right after this part
                 pk = 0;
-                --pleft;
+                if (ph > 0 && has_part(pr, 0)) {
+                    ph = 0;
+                } else {
+                    ++pr;
+                    ph = has_part(pr, P - 1) ? P - 1 : 0;
+                }
             }
             return w;
         };
         uint4 qa = load_next(), qb = load_next();
-        __syncthreads();  // mbarrier inits and staged scales visible
+        // hand-off slots for split rows: slot w = lane state of the row whose part 1 starts
+        // warp w's range (NV2 floats per lane), flag[w] = 1 once written
+        float* slot = reinterpret_cast<float*>(smem + SL.slot_off);
+        int* flag = reinterpret_cast<int*>(smem + SL.cnt_off);
+        if (threadIdx.x <= nwarps) flag[threadIdx.x] = 0;
+        __syncthreads();  // mbarrier inits, flags and staged scales visible
         trace(tslot, 1);
 #if WW_DEBUG_FLAGS
         if (!(p.dbg & 1))
@@ -559,15 +588,13 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         const uint32_t xb0 = xs + (uint32_t)lane * 128u, xpart = (uint32_t)(B * J * 4096);
         const uint32_t bstride = (uint32_t)J * 4096u;
         uint32_t seen = 0;  // bit h: the x slices of part h have been waited for
-        float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][P][NV]
-#pragma unroll 1
-        for (int u = u0; u < u1; ++u) {
-            const int ch = u & (P - 1);  // part (P is a power of two)
-            if (!((seen >> ch) & 1u)) {  // first unit of this part: its x slices must be in
-                for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * (ch * J + j));
-                seen |= 1u << ch;
+        float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][NV]
+        auto sweep_part = [&](int h) {
+            if (!((seen >> h) & 1u)) {  // first unit of this part: its x slices must be in
+                for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * (h * J + j));
+                seen |= 1u << h;
             }
-            uint32_t xc = (xb0 + (uint32_t)ch * xpart) | l7;
+            uint32_t xc = (xb0 + (uint32_t)h * xpart) | l7;
 #pragma unroll 1
             for (int k = 0; k < J; ++k) {
                 const uint4 cur = qa;
@@ -580,26 +607,47 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                     chunk<B>(acc, cur, xc, bstride);
                 xc += 4096u;
             }
-            // reduce this part over the lanes (a7) into the CTA's totals
-            reduce_to<B>(acc, tot + u * NV);
+        };
+#pragma unroll 1
+        for (int r = ra; r <= rz; ++r) {
+            if (P > 1 && has_part(r, 1)) {
+                sweep_part(1);
+                if (!has_part(r, 0)) {  // part 0 is the previous warp's: hand the state over
+                    acc.store(slot + warp * Acc<B>::kFloats * 32, lane);
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        *reinterpret_cast<volatile int*>(flag + warp) = 1;
+                    }
+                    acc.zero();
+                    continue;
+                }
+            } else if (P > 1) {  // part 1 was the next warp's first unit: continue its state
+                if (lane == 0)
+                    while (*reinterpret_cast<volatile int*>(flag + warp + 1) == 0) {
+                    }
+                __syncwarp();
+                __threadfence_block();
+                acc.load(slot + (warp + 1) * Acc<B>::kFloats * 32, lane);
+            }
+            sweep_part(0);
+            // reduce the row over the lanes (a7) into the CTA's totals
+            reduce_to<B>(acc, tot + r * NV);
             if (tr_sweep < 29) trace(tslot, tr_sweep++);
             acc.zero();
         }
         trace(tslot, 29);  // sweeps done
         // Epilogue (a8) for all rows of the CTA at once: thread t takes (row, vector) items
-        // t, t + blockDim, ...: row total = ((part 0 + part 1) + part 2) + part 3 (in that
-        // order), 8 scale multiplies, one coalesced complex64 store per item.
+        // t, t + blockDim, ...: 8 scale multiplies on the row's totals, one coalesced
+        // complex64 store per item.
         __syncthreads();
         const int NR = (int)(r1 - r0);
         for (int it = threadIdx.x; it < NR * B; it += blockDim.x) {
             const int b = it / NR, lr = it - b * NR;
-            const float* T0 = tot + (lr * P) * NV + 8 * b;
+            const float* T0 = tot + lr * NV + 8 * b;
             float T[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) T[i] = T0[i];
-            for (int h = 1; h < P; ++h)
-#pragma unroll
-                for (int i = 0; i < 8; ++i) T[i] += T0[h * NV + i];
             const float* sr = reinterpret_cast<const float*>(smem + SL.scale_off) +
                               (p.per_row_scales ? 4 * lr : 0);
             store_y(p, T, sr, b, r0 + lr);
@@ -696,12 +744,11 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     const int64_t grid = std::min<int64_t>(sms, L->n);
     const int64_t rows = (L->n + grid - 1) / grid;  // rows per CTA (at most)
     // Single x tile: a row is split into P = 2 equal column parts of >= 64 chunks (2 sweeps)
-    // when W is even, else P = 1; the choice depends on (m, B) only (x must
-    // fit kXBudgetBytes).  (P = 4 for m = 5504 measured slower: the extra part reductions
-    // cost more than the finer balance gains; the kernel supports any power of two.)
+    // when W is even and B <= 2 (the split-row hand-off carries the lane accumulators), else
+    // P = 1; the choice depends on (m, B) only (x must fit kXBudgetBytes).
     int parts = 1;
     for (int cand : {2})
-        if (W % cand == 0 && W / cand >= 64 &&
+        if (B <= 2 && W % cand == 0 && W / cand >= 64 &&
             (int64_t)B * 32 * cand * ((W / cand + 31) / 32) * 128 <= kXBudgetBytes) {
             parts = cand;
             break;
