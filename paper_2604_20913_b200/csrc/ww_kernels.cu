@@ -26,6 +26,9 @@
 #include "ww.h"
 #include "ww_internal.h"
 
+#ifndef WW_UNROLL2
+#define WW_UNROLL2 0  // 1: two sweeps per loop iteration (A/B builds; measured 3% slower)
+#endif
 #ifndef WW_DEBUG_FLAGS
 #define WW_DEBUG_FLAGS 0  // 1: honour Params::dbg (tools/chain_time.py builds build/libww_dbg.so)
 #endif
@@ -528,6 +531,11 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         const int len = p.split;                           // chunks per part
         const int J = p.J0;                                // sweeps per part
         const bool lastok = lane < len - 32 * (J - 1);     // lane active in a part's last sweep
+#if WW_UNROLL2
+        const int Jp = (J + 1) & ~1;  // sweeps are taken in pairs; an odd J gets an empty one
+#else
+        const int Jp = J;
+#endif
         // rows touched by this warp: [ra, rz]; with P == 2 the first may lack part 0 (its
         // part 0 is the previous warp's) and the last may lack part 1 (the next warp's)
         const int ra = u0 / P, rz = (u1 - 1) / P;
@@ -548,18 +556,27 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         // two sweeps ahead, the first two issued before griddepcontrol.wait (weights never
         // depend on the previous kernel).  Lanes past a part's end load zeros, so no predicate
         // fires for them.
+        // producer position: row pr, part ph, sweep pk; pptr = this lane's chunk of the sweep
+        // (advanced incrementally: +32 chunks per sweep, one jump per part)
         int pr = ra, ph = has_part(ra, P - 1) ? P - 1 : 0, pk = 0;
+        bool plive = ra <= rz;
+        const uint4* pptr = p.packed + (r0 + ra) * p.W + ph * len + lane;
+        const int64_t Wl = p.W;
         auto load_next = [&]() -> uint4 {
-            const uint4* q = p.packed + (r0 + pr) * p.W + ph * len + 32 * pk + lane;
-            const uint4 w = ldg_stream_if(q, pr <= rz && (pk < J - 1 || lastok));
-            if (++pk == J) {
+            const uint4 w = ldg_stream_if(pptr, plive && (pk < J - 1 || (pk == J - 1 && lastok)));
+            pptr += 32;
+            if (++pk == Jp) {  // next part: part 0 of this row, else part P-1 of the next row
                 pk = 0;
+                pptr -= 32 * Jp + ph * len;  // back to the start of this part's row
                 if (ph > 0 && has_part(pr, 0)) {
                     ph = 0;
                 } else {
                     ++pr;
                     ph = has_part(pr, P - 1) ? P - 1 : 0;
+                    pptr += Wl;
+                    plive = pr <= rz;
                 }
+                pptr += ph * len;
             }
             return w;
         };
@@ -595,6 +612,25 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 seen |= 1u << h;
             }
             uint32_t xc = (xb0 + (uint32_t)h * xpart) | l7;
+#if WW_UNROLL2
+            // two sweeps per iteration with fixed registers: qa / qb are each refilled right
+            // after their chunk (one sweep of prefetch distance, no register moves)
+#pragma unroll 1
+            for (int k = 0; k < Jp; k += 2) {
+                if (tr_sweep < 29) trace(tslot, tr_sweep++);
+#if WW_DEBUG_FLAGS
+                if (!(p.dbg & 2))
+#endif
+                    chunk<B>(acc, qa, xc, bstride);
+                qa = load_next();
+#if WW_DEBUG_FLAGS
+                if (!(p.dbg & 2))
+#endif
+                    chunk<B>(acc, qb, xc + 4096u, bstride);
+                qb = load_next();
+                xc += 8192u;
+            }
+#else
 #pragma unroll 1
             for (int k = 0; k < J; ++k) {
                 const uint4 cur = qa;
@@ -607,6 +643,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                     chunk<B>(acc, cur, xc, bstride);
                 xc += 4096u;
             }
+#endif
         };
 #pragma unroll 1
         for (int r = ra; r <= rz; ++r) {
