@@ -26,6 +26,12 @@
 #include "ww.h"
 #include "ww_internal.h"
 
+#ifndef WW_S2_MAXB
+#define WW_S2_MAXB 2  // batch sizes with two column-parity accumulator sets
+#endif
+#ifndef WW_2CTA_MAXB
+#define WW_2CTA_MAXB 1  // batch sizes capped at 64 registers (two CTAs per SM)
+#endif
 #ifndef WW_UNROLL2
 #define WW_UNROLL2 0  // 1: two sweeps per loop iteration (A/B builds; measured 3% slower)
 #endif
@@ -273,7 +279,7 @@ __device__ __forceinline__ void stage_x_regions_tma(const Params& p, uint32_t xs
 #endif
 template <int B>
 struct Acc {
-    static constexpr int S = B <= 2 ? 2 : 1;  // column-parity sets
+    static constexpr int S = B <= WW_S2_MAXB ? 2 : 1;  // column-parity sets
     static constexpr int N = WW_ACC_N;
     float2 a[S][N][B][4];
     __device__ __forceinline__ void zero() {
@@ -448,7 +454,7 @@ struct SmemLayout {
 __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
                                                   int nbars, int rows, int parts) {
     const int64_t nv = next_pow2(8 * B);
-    const int64_t acc_floats = (B <= 2 ? 2 : 1) * B * 8;  // Acc<B>::kFloats
+    const int64_t acc_floats = (B <= WW_S2_MAXB ? 2 : 1) * B * 8;  // Acc<B>::kFloats
     SmemLayout L;
     L.x_bytes = (int64_t)B * x_chunks * 128;
     L.scratch_off = L.x_bytes;
@@ -464,7 +470,7 @@ __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps
 // register cap: B == 1 keeps <= 64 registers so two CTAs fit an SM and a PDL-launched next
 // layer can start on every SM while this one drains
 template <int B>
-__host__ __device__ constexpr int min_blocks() { return B == 1 ? 2 : 1; }
+__host__ __device__ constexpr int min_blocks() { return B <= WW_2CTA_MAXB ? 2 : 1; }
 
 template <int B>
 __global__ void __launch_bounds__(warps_for<B>() * 32, min_blocks<B>())
@@ -598,13 +604,13 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         } else {
             stage_x_regions_cp_async<B>(p, xs, bars);
         }
+        uint32_t seen = 0;  // bit h: the x slices of part h have been waited for
         trace(tslot, 3);
         int tr_sweep = 4;
 
         const uint32_t l7 = (uint32_t)(lane & 7) << 4;  // swizzle key of the lane's chunks
         const uint32_t xb0 = xs + (uint32_t)lane * 128u, xpart = (uint32_t)(B * J * 4096);
         const uint32_t bstride = (uint32_t)J * 4096u;
-        uint32_t seen = 0;  // bit h: the x slices of part h have been waited for
         float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][NV]
         auto sweep_part = [&](int h) {
             if (!((seen >> h) & 1u)) {  // first unit of this part: its x slices must be in
