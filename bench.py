@@ -450,7 +450,7 @@ class _ReplicaLayer:
                 n = self.Y[0].numel() // self.world
                 dist.all_gather_into_tensor(self.Y[0], self.Y[0][self.rank * n:(self.rank + 1) * n],
                                             group=self.group)
-        return self.R
+        return self.R * self.ww.launches_for_batch(self.B)
 
     def algorithmic_bytes(self):
         m, n, B = self.spec.m, self.nloc, self.B

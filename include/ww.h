@@ -113,7 +113,9 @@ ww_status ww_wl_gemv(const ww_layer* L, const void* packed_d, const float* scale
 
 /* Batched small-B variant, 1 <= B <= WW_MAX_BATCH: X_d is B rows of m complex64 with row
  * stride ldx (complex elements, >= m); Y_d is B rows of n complex64 with stride ldy
- * (>= n).  Every decoded code drives all B vectors (one pass over the weights). */
+ * (>= n).  Every decoded code drives all the vectors of a launch (one pass over the
+ * weights per launch); B > 4 runs as groups of 4 vectors, one launch each (the last group
+ * may overlap the previous one), so ww_query_launch(L, B > 4) describes one group. */
 ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d, const float* scales_d,
                              const float* X_d, int64_t ldx, float* Y_d, int64_t ldy, int32_t B,
                              void* stream);

@@ -191,6 +191,14 @@ def wl_gemv(layer: Layer, packed, scales, x, y=None, stream=None):
     return y
 
 
+GROUP = 4  # ww.h: batches above 4 vectors run as groups of 4, one launch each
+
+
+def launches_for_batch(B: int) -> int:
+    """Kernel launches one ww_wl_gemv_batched call makes for B vectors."""
+    return 1 if B <= GROUP else -(-B // GROUP)
+
+
 def wl_gemv_batched(layer: Layer, packed, scales, X, Y=None, stream=None):
     """Y[b] = WL-GEMV(X[b]) for a (B, m) complex64 CUDA tensor (row stride X.stride(0))."""
     import torch

@@ -48,6 +48,7 @@ template <int B>
 __host__ __device__ constexpr int warps_for() { return B <= 4 ? 16 : 8; }
 inline int warps_for_b(int B) { return B <= 4 ? 16 : 8; }
 constexpr int kXBudgetBytes = 184 * 1024;  // x tile per CTA (multi-tile path)
+constexpr int kGroup = 4;                  // batches above this run as groups of 4 vectors
 constexpr int64_t kSmemBudget = 226 * 1024; // single-tile path: all shared memory of a CTA
 
 // ------------------------------------------------------------------ PTX helpers
@@ -935,7 +936,7 @@ extern "C" ww_status ww_query_launch(const ww_layer* L, int32_t B, ww_launch_inf
     if (!out) return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_query_launch: null out");
     if (B < 1 || B > WW_MAX_BATCH)
         return ww::fail(WW_ERR_UNSUPPORTED, "ww_query_launch: B=%d", B);
-    plan(L, B, num_sms(), out);
+    plan(L, B > kGroup ? kGroup : B, num_sms(), out);  // B > 4: one launch per group of 4
     return ww::ok();
 }
 
@@ -945,26 +946,11 @@ extern "C" int ww_debug_set_trace(void* dev_ptr) {
 }
 #endif
 
-extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
-                                        const float* scales_d, const float* X_d, int64_t ldx,
-                                        float* Y_d, int64_t ldy, int32_t B, void* stream) {
-    ww_status st = check_layer(L, "ww_wl_gemv");
-    if (st != WW_OK) return st;
-    if (!packed_d || !scales_d || !X_d || !Y_d)
-        return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_wl_gemv: null pointer");
-    if (B < 1) return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_wl_gemv: B=%d", B);
-    if (B > WW_MAX_BATCH)
-        return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv: B=%d > %d", B, WW_MAX_BATCH);
-    if (ldx < L->m || ldy < L->n)
-        return ww::fail(WW_ERR_DIMENSION_MISMATCH, "ww_wl_gemv: ldx=%lld (m=%lld) ldy=%lld (n=%lld)",
-                        (long long)ldx, (long long)L->m, (long long)ldy, (long long)L->n);
-    if (((uintptr_t)packed_d & 15) || ((uintptr_t)X_d & 7) || ((uintptr_t)Y_d & 7) ||
-        ((uintptr_t)scales_d & 3))
-        return ww::fail(WW_ERR_MISALIGNED, "ww_wl_gemv: packed must be 16-B, x/y 8-B aligned");
-    const char* xb = reinterpret_cast<const char*>(X_d);
-    const char* yb = reinterpret_cast<const char*>(Y_d);
-    if (xb < yb + 8 * (ldy * (B - 1) + L->n) && yb < xb + 8 * (ldx * (B - 1) + L->m))
-        return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_wl_gemv: x and y overlap");
+namespace {
+// one launch of wl_gemv_kernel<B> (arguments already validated)
+ww_status launch_batch(const ww_layer* L, const void* packed_d, const float* scales_d,
+                       const float* X_d, int64_t ldx, float* Y_d, int64_t ldy, int32_t B,
+                       void* stream) {
     ww_launch_info li;
     plan(L, B, num_sms(), &li);
     Params p;
@@ -995,6 +981,44 @@ extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
     if (e != cudaSuccess)
         return ww::fail(WW_ERR_CUDA, "ww_wl_gemv: launch failed: %s", cudaGetErrorString(e));
     return ww::ok();
+}
+}  // namespace
+
+extern "C" ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d,
+                                        const float* scales_d, const float* X_d, int64_t ldx,
+                                        float* Y_d, int64_t ldy, int32_t B, void* stream) {
+    ww_status st = check_layer(L, "ww_wl_gemv");
+    if (st != WW_OK) return st;
+    if (!packed_d || !scales_d || !X_d || !Y_d)
+        return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_wl_gemv: null pointer");
+    if (B < 1) return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_wl_gemv: B=%d", B);
+    if (B > WW_MAX_BATCH)
+        return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv: B=%d > %d", B, WW_MAX_BATCH);
+    if (ldx < L->m || ldy < L->n)
+        return ww::fail(WW_ERR_DIMENSION_MISMATCH, "ww_wl_gemv: ldx=%lld (m=%lld) ldy=%lld (n=%lld)",
+                        (long long)ldx, (long long)L->m, (long long)ldy, (long long)L->n);
+    if (((uintptr_t)packed_d & 15) || ((uintptr_t)X_d & 7) || ((uintptr_t)Y_d & 7) ||
+        ((uintptr_t)scales_d & 3))
+        return ww::fail(WW_ERR_MISALIGNED, "ww_wl_gemv: packed must be 16-B, x/y 8-B aligned");
+    const char* xb = reinterpret_cast<const char*>(X_d);
+    const char* yb = reinterpret_cast<const char*>(Y_d);
+    if (xb < yb + 8 * (ldy * (B - 1) + L->n) && yb < xb + 8 * (ldx * (B - 1) + L->m))
+        return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_wl_gemv: x and y overlap");
+    if (B > kGroup) {
+        // groups of kGroup vectors, one launch each (the last group may overlap the previous
+        // one and rewrite identical values): a vector's accumulation order is the same in
+        // every group of the B >= 3 family, and the weights are streamed once per group --
+        // cheaper than one launch over all B (x beyond one tile, 255 registers, 8 warps)
+        for (int32_t g0 = 0; g0 < B; g0 += kGroup) {
+            const int32_t s0 = g0 + kGroup <= B ? g0 : B - kGroup;
+            const ww_status gs = launch_batch(L, packed_d, scales_d, X_d + 2 * s0 * ldx, ldx,
+                                              Y_d + 2 * s0 * ldy, ldy, kGroup, stream);
+            if (gs != WW_OK) return gs;
+            if (s0 + kGroup >= B) break;
+        }
+        return ww::ok();
+    }
+    return launch_batch(L, packed_d, scales_d, X_d, ldx, Y_d, ldy, B, stream);
 }
 
 extern "C" ww_status ww_wl_gemv(const ww_layer* L, const void* packed_d, const float* scales_d,

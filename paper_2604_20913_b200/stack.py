@@ -23,8 +23,8 @@ import torch
 
 import ww_inputs as wi
 
-from . import (CONV_EQ1, FLAG_PDL, LAYOUT_COL4, SCALES_PER_ROW, Layer, packed_bytes,
-               pack_ternary_device, shard_plan, wl_gemv_batched)
+from . import (CONV_EQ1, FLAG_PDL, LAYOUT_COL4, SCALES_PER_ROW, Layer, launches_for_batch,
+               packed_bytes, pack_ternary_device, shard_plan, wl_gemv_batched)
 
 PROJ_NAMES = ("q", "k", "v", "o", "gate", "up", "down")
 FUSED_STAGES = (("qkv", (0, 1, 2)), ("o", (3,)), ("gateup", (4, 5)), ("down", (6,)))
@@ -170,7 +170,7 @@ class WLStack:
         wl_gemv_batched(L, self.W[st.off:st.off + st.nbytes],
                         self.S[st.soff:st.soff + 4 * st.ylocal], self.x_of(st),
                         self.y_local_view(st), stream=stream)
-        return 1
+        return launches_for_batch(self.B)
 
     def exchange(self, i: int):
         """All-gather of stage i's y shards (NCCL over NVLink); no-op on one rank."""

@@ -156,7 +156,9 @@ def test_query_launch_shapes():
         assert li["grid"] >= 1 and li["block"] % 32 == 0
         assert li["tiles"] == 1
         assert li["tile_chunks"] == -(-m // 16)
-    li = ww.query_launch(ww.Layer(2048, 5504), 16)
+    # B > 4 runs as groups of 4 vectors: the plan of one group
+    assert ww.query_launch(ww.Layer(2048, 5504), 16) == ww.query_launch(ww.Layer(2048, 5504), 4)
+    li = ww.query_launch(ww.Layer(2048, 8000), 4)  # x of 4 vectors beyond one tile
     assert li["tiles"] > 1 and li["tile_chunks"] % 32 == 0
     with pytest.raises(ww.WWError) as e:
         ww.query_launch(ww.Layer(8, 8), 17)

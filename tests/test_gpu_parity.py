@@ -73,10 +73,24 @@ def test_multi_tile_long_rows():
 
 
 def test_batched_multi_tile_and_waves():
-    # B=16 on 2048 x 5504 uses column tiles; 5000 rows forces several row waves per CTA
-    case = LayerCase(5000, 3000, seed=4, B=16).device(ww, torch)
-    assert ww.query_launch(case.layer(ww, 0), 16)["tiles"] > 1
+    # 4 vectors of 8000 columns need column tiles; 5000 rows force several row waves per CTA
+    case = LayerCase(5000, 8000, seed=4, B=4).device(ww, torch)
+    assert ww.query_launch(case.layer(ww, 0), 4)["tiles"] > 1
     assert_parity(case.gpu(ww, torch, ww.CONV_ALG1), case.oracle(orc.CONV_ALG1), case)
+
+
+@pytest.mark.parametrize("B", [5, 6, 7, 8, 13, 16])
+def test_large_batches_run_as_groups_bitwise_equal_to_group_launches(B):
+    # B > 4 runs as groups of 4 vectors (the last group overlapping): every vector equals a
+    # launch of its own group of 4, bitwise, and matches the oracle
+    case = LayerCase(700, 2100, seed=B, B=B).device(ww, torch)
+    yb = case.gpu(ww, torch, ww.CONV_EQ1)
+    assert_parity(yb, case.oracle(orc.CONV_EQ1), case)
+    L = case.layer(ww, ww.CONV_EQ1)
+    for b in range(B):
+        s0 = min(b - b % 4, B - 4)
+        y4 = ww.wl_gemv_batched(L, case.packed_d, case.scales_d, case.x_d[s0:s0 + 4])
+        assert np.array_equal(y4[b - s0].cpu().numpy(), yb[b])
 
 
 def test_zero_and_identity_exact():
