@@ -61,7 +61,7 @@ class _Shard(ctypes.Structure):
 
 class _LaunchInfo(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in ("grid", "block", "smem_bytes", "tiles",
-                                              "tile_chunks", "num_sms", "parts", "split_chunks")]
+                                              "tile_chunks", "num_sms", "parts", "split_chunks", "path")]
 
 
 _i64, _i32, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p

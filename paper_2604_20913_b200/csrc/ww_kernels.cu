@@ -139,6 +139,7 @@ struct alignas(64) Params {
     int32_t per_row_scales, conv, tile_chunks, ntiles, aligned16;
     int32_t x_stride;     // multi-tile path: chunks per vector in the shared x tile
     int32_t use_tma;      // stage x with cp.async.bulk.tensor (else per-thread cp.async)
+    int32_t single;       // 1: single x tile path (ww_launch_info.path == 0)
     int32_t parts;        // single-tile path: equal column parts per row (1, 2 or 4), plan()
     int32_t split;        // chunks per part (W / parts)
     int32_t J0;           // 32-chunk sweeps (= x slices) per part
@@ -483,7 +484,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     unsigned char* smem = smem_raw + (xs - raw);
     const int nwarps = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool single = p.ntiles == 1;
+    const bool single = p.single != 0;
     const int nbars = single ? p.parts * p.J0 : 0;
     const SmemLayout SL = smem_layout(B, single ? 32 * p.parts * p.J0 : p.x_stride, nwarps,
                                       single, nbars, p.rows_cap, p.parts);
@@ -813,15 +814,18 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
         li->parts = parts;
         li->split_chunks = (int32_t)split;
         li->smem_bytes = (int32_t)single_bytes(parts, split);
+        li->path = 0;
         return WW_OK;
     }
-    // x does not fit: column tiles of whole 32-chunk sweeps, one part per row
+    // x (or the CTA's row totals) does not fit one tile: column tiles of whole 32-chunk
+    // sweeps, one part per row, row waves
     int64_t tc = kXBudgetBytes / ((int64_t)B * 128);
-    tc = std::max<int64_t>(32, tc / 32 * 32);
+    tc = std::min<int64_t>(std::max<int64_t>(32, tc / 32 * 32), (W + 31) / 32 * 32);
     li->tile_chunks = (int32_t)tc;
     li->tiles = (int32_t)((W + tc - 1) / tc);
     li->parts = 1;
     li->split_chunks = (int32_t)W;
+    li->path = 1;
     li->smem_bytes = (int32_t)smem_layout(B, (int)tc, warps, false, 0, 0, 1).total;
     return WW_OK;
 }
@@ -974,7 +978,8 @@ ww_status launch_batch(const ww_layer* L, const void* packed_d, const float* sca
     p.rows_cap = (int32_t)((L->n + li.grid - 1) / li.grid);
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
     p.x_stride = (li.tile_chunks + 31) / 32 * 32;
-    p.use_tma = li.tiles == 1 && !g_force_cp_async ? (encode_x_map(p, B) ? 1 : 0) : 0;
+    p.single = li.path == 0;
+    p.use_tma = p.single && !g_force_cp_async ? (encode_x_map(p, B) ? 1 : 0) : 0;
     p.dbg = g_debug_flags;
     g_last_use_tma = p.use_tma;
     cudaError_t e = launch(p, li, B, (cudaStream_t)stream, (L->flags & WW_FLAG_PDL) != 0);

@@ -265,3 +265,15 @@ def test_unfused_ablation_matches_oracle(n, m, conv):
     y = ww.wl_gemv_unfused(L, planar, case.scales_d, case.x_d[0])
     torch.cuda.synchronize()
     assert_parity(y.cpu().numpy()[None], case.oracle(ORC[conv]), case)
+
+
+@pytest.mark.parametrize("n", [200_000, 800_000])
+def test_many_rows_per_cta(n):
+    # 1,350 rows per CTA still fit the shared totals (one tile); 5,400 do not, and the launch
+    # takes the row-wave path -- both match the oracle
+    m = 24
+    case = LayerCase(n, m, seed=77).device(ww, torch)
+    li = ww.query_launch(case.layer(ww, 0), 1)
+    assert li["path"] == (0 if n == 200_000 else 1)
+    for conv in CONVS:
+        assert_parity(case.gpu(ww, torch, conv), case.oracle(ORC[conv]), case)
