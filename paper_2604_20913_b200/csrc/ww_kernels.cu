@@ -26,15 +26,6 @@
 #include "ww.h"
 #include "ww_internal.h"
 
-#ifndef WW_S2_MAXB
-#define WW_S2_MAXB 2  // batch sizes with two column-parity accumulator sets
-#endif
-#ifndef WW_2CTA_MAXB
-#define WW_2CTA_MAXB 1  // batch sizes capped at 64 registers (two CTAs per SM)
-#endif
-#ifndef WW_UNROLL2
-#define WW_UNROLL2 0  // 1: two sweeps per loop iteration (A/B builds; measured 3% slower)
-#endif
 #ifndef WW_DEBUG_FLAGS
 #define WW_DEBUG_FLAGS 0  // 1: honour Params::dbg (tools/chain_time.py builds build/libww_dbg.so)
 #endif
@@ -272,17 +263,14 @@ __device__ __forceinline__ void stage_x_regions_tma(const Params& p, uint32_t xs
     }
 }
 
-// Accumulators: S column-parity sets of B x 4 pair sums (N = 2: separate sums of the +1 and
-// the -1 codes, combined as pos - neg at the end).  For B <= 2 even and odd columns feed
-// separate sets (more independent FADD2 chains per warp, half-length fp32 chains); larger
-// B has ILP across vectors.
-#ifndef WW_ACC_N
-#define WW_ACC_N 1
-#endif
+// Accumulators: S column-parity sets of B x 4 pair sums.  For B <= 2 even and odd columns
+// feed separate sets (more independent FADD2 chains per warp, half-length fp32 chains);
+// larger B has ILP across vectors.  (Separate sums of the +1 and the -1 codes measured
+// 5-10 % slower: register pressure.)
 template <int B>
 struct Acc {
-    static constexpr int S = B <= WW_S2_MAXB ? 2 : 1;  // column-parity sets
-    static constexpr int N = WW_ACC_N;
+    static constexpr int S = B <= 2 ? 2 : 1;  // column-parity sets
+    static constexpr int N = 1;
     float2 a[S][N][B][4];
     __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -456,7 +444,7 @@ struct SmemLayout {
 __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
                                                   int nbars, int rows, int parts) {
     const int64_t nv = next_pow2(8 * B);
-    const int64_t acc_floats = (B <= WW_S2_MAXB ? 2 : 1) * B * 8;  // Acc<B>::kFloats
+    const int64_t acc_floats = (B <= 2 ? 2 : 1) * B * 8;  // Acc<B>::kFloats
     SmemLayout L;
     L.x_bytes = (int64_t)B * x_chunks * 128;
     L.scratch_off = L.x_bytes;
@@ -472,7 +460,7 @@ __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps
 // register cap: B == 1 keeps <= 64 registers so two CTAs fit an SM and a PDL-launched next
 // layer can start on every SM while this one drains
 template <int B>
-__host__ __device__ constexpr int min_blocks() { return B <= WW_2CTA_MAXB ? 2 : 1; }
+__host__ __device__ constexpr int min_blocks() { return B == 1 ? 2 : 1; }
 
 template <int B>
 __global__ void __launch_bounds__(warps_for<B>() * 32, min_blocks<B>())
@@ -539,11 +527,6 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         const int len = p.split;                           // chunks per part
         const int J = p.J0;                                // sweeps per part
         const bool lastok = lane < len - 32 * (J - 1);     // lane active in a part's last sweep
-#if WW_UNROLL2
-        const int Jp = (J + 1) & ~1;  // sweeps are taken in pairs; an odd J gets an empty one
-#else
-        const int Jp = J;
-#endif
         // rows touched by this warp: [ra, rz]; with P == 2 the first may lack part 0 (its
         // part 0 is the previous warp's) and the last may lack part 1 (the next warp's)
         const int ra = u0 / P, rz = (u1 - 1) / P;
@@ -571,11 +554,12 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         const uint4* pptr = p.packed + (r0 + ra) * p.W + ph * len + lane;
         const int64_t Wl = p.W;
         auto load_next = [&]() -> uint4 {
+            // (pk == J - 1 spelled out: this form measured faster -- codegen)
             const uint4 w = ldg_stream_if(pptr, plive && (pk < J - 1 || (pk == J - 1 && lastok)));
             pptr += 32;
-            if (++pk == Jp) {  // next part: part 0 of this row, else part P-1 of the next row
+            if (++pk == J) {  // next part: part 0 of this row, else part P-1 of the next row
                 pk = 0;
-                pptr -= 32 * Jp + ph * len;  // back to the start of this part's row
+                pptr -= 32 * J + ph * len;  // back to the start of this part's row
                 if (ph > 0 && has_part(pr, 0)) {
                     ph = 0;
                 } else {
@@ -620,25 +604,6 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 seen |= 1u << h;
             }
             uint32_t xc = (xb0 + (uint32_t)h * xpart) | l7;
-#if WW_UNROLL2
-            // two sweeps per iteration with fixed registers: qa / qb are each refilled right
-            // after their chunk (one sweep of prefetch distance, no register moves)
-#pragma unroll 1
-            for (int k = 0; k < Jp; k += 2) {
-                if (tr_sweep < 29) trace(tslot, tr_sweep++);
-#if WW_DEBUG_FLAGS
-                if (!(p.dbg & 2))
-#endif
-                    chunk<B>(acc, qa, xc, bstride);
-                qa = load_next();
-#if WW_DEBUG_FLAGS
-                if (!(p.dbg & 2))
-#endif
-                    chunk<B>(acc, qb, xc + 4096u, bstride);
-                qb = load_next();
-                xc += 8192u;
-            }
-#else
 #pragma unroll 1
             for (int k = 0; k < J; ++k) {
                 const uint4 cur = qa;
@@ -651,7 +616,6 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                     chunk<B>(acc, cur, xc, bstride);
                 xc += 4096u;
             }
-#endif
         };
 #pragma unroll 1
         for (int r = ra; r <= rz; ++r) {
