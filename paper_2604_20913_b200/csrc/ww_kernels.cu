@@ -51,14 +51,14 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     return v;
 }
 
-// the same load, issued only when `pred` holds (else zeros): one predicated LDG, no branch
-__device__ __forceinline__ uint4 ldg_stream_if(const uint4* p, bool pred) {
+// the same load, issued only when a < b (else zeros): one compare + one predicated LDG
+__device__ __forceinline__ uint4 ldg_stream_lt(const uint4* p, int a, int b) {
     uint4 v = make_uint4(0, 0, 0, 0);
     asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %5, %6;\n\t"
         "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
         : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-        : "l"(p), "r"((int)pred));
+        : "l"(p), "r"(a), "r"(b));
     return v;
 }
 
@@ -550,12 +550,14 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         // producer position: row pr, part ph, sweep pk; pptr = this lane's chunk of the sweep
         // (advanced incrementally: +32 chunks per sweep, one jump per part)
         int pr = ra, ph = has_part(ra, P - 1) ? P - 1 : 0, pk = 0;
-        bool plive = ra <= rz;
+        // sweep pk of a part is loaded iff pk < kv: kv = J on lanes active in the part's last
+        // sweep, J - 1 on the others, 0 past the warp's last row (one compare per sweep)
+        const int kvl = lastok ? J : J - 1;
+        int kv = ra <= rz ? kvl : 0;
         const uint4* pptr = p.packed + (r0 + ra) * p.W + ph * len + lane;
         const int64_t Wl = p.W;
         auto load_next = [&]() -> uint4 {
-            // (pk == J - 1 spelled out: this form measured faster -- codegen)
-            const uint4 w = ldg_stream_if(pptr, plive && (pk < J - 1 || (pk == J - 1 && lastok)));
+            const uint4 w = ldg_stream_lt(pptr, pk, kv);
             pptr += 32;
             if (++pk == J) {  // next part: part 0 of this row, else part P-1 of the next row
                 pk = 0;
@@ -566,7 +568,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                     ++pr;
                     ph = has_part(pr, P - 1) ? P - 1 : 0;
                     pptr += Wl;
-                    plive = pr <= rz;
+                    kv = pr <= rz ? kvl : 0;
                 }
                 pptr += ph * len;
             }
