@@ -137,12 +137,12 @@ ww_status ww_shard_plan(int64_t n, int64_t m, int32_t world, int32_t rank, ww_sh
 
 /* Launch configuration the GPU entry points use for (L, B): grid (one CTA per SM, each
  * owning a contiguous row range), block, dynamic shared memory, the number of x column
- * tiles and their width (16-column chunks), the SM count it was planned for, the
- * column parts of a row (1 or 2; part 0 = the first split_chunks chunks) and the path
- * (0 = single x tile; 1 = column tiles with row waves, taken when x or the CTA's row
- * totals do not fit shared memory).  The parts are a
- * function of (m, B) only: each part is warp-reduced on its own and the row total is
- * part 0 + part 1, so results never depend on n, the shard or the grid.  Pure host function. */
+ * tiles and their width (16-column chunks), the SM count it was planned for, the column
+ * parts of a row (always 1 and split_chunks = W = ceil(m/16) in this version: a row is
+ * one warp's work unit, swept 32 chunks at a time) and the path (0 = single x tile; 1 =
+ * column tiles with row waves, taken when x or the CTA's row totals do not fit shared
+ * memory).  A row's accumulation order is a function of (m, B) only, so results never
+ * depend on n, the shard or the grid.  Pure host function. */
 typedef struct {
     int32_t grid, block, smem_bytes, tiles, tile_chunks, num_sms, parts, split_chunks, path;
 } ww_launch_info;

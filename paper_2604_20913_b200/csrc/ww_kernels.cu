@@ -131,9 +131,7 @@ struct alignas(64) Params {
     int32_t x_stride;     // multi-tile path: chunks per vector in the shared x tile
     int32_t use_tma;      // stage x with cp.async.bulk.tensor (else per-thread cp.async)
     int32_t single;       // 1: single x tile path (ww_launch_info.path == 0)
-    int32_t parts;        // single-tile path: equal column parts per row (1, 2 or 4), plan()
-    int32_t split;        // chunks per part (W / parts)
-    int32_t J0;           // 32-chunk sweeps (= x slices) per part
+    int32_t J;            // single-tile path: 32-chunk sweeps (= x slices) per row
     int32_t rows_cap;     // single-tile path: rows per CTA the shared totals / scales hold
     int32_t dbg;          // tools only (ww_debug_set_flags): 1 = skip griddepcontrol.wait,
                           // bits 8..: trace slot (WW_TRACE builds),
@@ -219,47 +217,39 @@ __device__ __forceinline__ void stage_x(const Params& p, uint32_t xs, int64_t c0
     }
 }
 
-// Single-tile x staging.  Part h of the row (chunks [h*len, (h+1)*len)) has its own x region
-// at xs + h*B*J*4096: vector b's 32*J chunks at + b*J*4096, chunk c (relative to the part) at
-// + c*128, granules swizzled by (c & 7) -- the 128B-swizzle TMA layout, since every region is
-// 1024-B aligned.  Slice j of part h = relative chunks [32j, 32j+32) of every vector,
-// completing mbarrier h*J + j.
+// Single-tile x staging: vector b's 32*J chunks at xs + b*J*4096, chunk c at + c*128,
+// granules swizzled by (c & 7) -- the 128B-swizzle TMA layout, since the region is 1024-B
+// aligned.  Slice j = chunks [32j, 32j+32) of every vector, completing mbarrier j.
 
 template <int B>
 __device__ __forceinline__ void stage_x_regions_cp_async(const Params& p, uint32_t xs,
                                                          uint32_t bars) {
-    const int J = p.J0, len = p.split;
-    for (int sl = 0; sl < p.parts * J; ++sl) {
-        const int h = sl / J, j = sl - h * J;
-        const uint32_t roff = (uint32_t)(h * B * J * 4096);
+    const int J = p.J;
+    for (int j = 0; j < J; ++j) {
         const int span = 32 * 8;  // granules per vector in one slice
         for (int t = threadIdx.x; t < B * span; t += blockDim.x) {
             const int b = B == 1 ? 0 : t / span;
             const int g = 32 * 8 * j + (B == 1 ? t : t - b * span);
-            const int tc = g >> 3, gg = g & 7;  // chunk relative to the part
-            const int64_t col = (int64_t)(h * len + tc) * 16 + 2 * gg;
-            const uint32_t dst =
-                xs + roff + (uint32_t)(((b * J * 32 + tc) * 8 + (gg ^ (tc & 7))) * 16);
-            // chunks past the part's end (padding of its last slice) are zero-filled
-            const int64_t valid = tc < len ? p.m - col : 0;
-            stage_granule(p, dst, p.X + 2 * (b * p.ldx + col), valid);
+            const int tc = g >> 3, gg = g & 7;
+            const int64_t col = (int64_t)tc * 16 + 2 * gg;
+            const uint32_t dst = xs + (uint32_t)(((b * J * 32 + tc) * 8 + (gg ^ (tc & 7))) * 16);
+            // columns past m (padding of the last slice) are zero-filled
+            stage_granule(p, dst, p.X + 2 * (b * p.ldx + col), p.m - col);
         }
-        cp_async_arrive(bars + 8 * sl);
+        cp_async_arrive(bars + 8 * j);
     }
 }
 
 // one thread per slice issues its TMA boxes (B of them), so all slices are in flight at once
 template <int B>
 __device__ __forceinline__ void stage_x_regions_tma(const Params& p, uint32_t xs, uint32_t bars) {
-    const int J = p.J0;
-    for (int sl = threadIdx.x; sl < p.parts * J; sl += blockDim.x) {
-        const int h = sl / J, j = sl - h * J;
-        const uint32_t bar = bars + 8 * sl;
+    const int J = p.J;
+    for (int j = threadIdx.x; j < J; j += blockDim.x) {
+        const uint32_t bar = bars + 8 * j;
         mbar_expect_tx(bar, (uint32_t)(B * 4096));
 #pragma unroll 1
         for (int b = 0; b < B; ++b)
-            tma_load_3d(xs + (uint32_t)(h * B * J * 4096 + (b * J + j) * 4096), &p.tmap, 0,
-                        h * p.split + 32 * j, b, bar);
+            tma_load_3d(xs + (uint32_t)((b * J + j) * 4096), &p.tmap, 0, 32 * j, b, bar);
     }
 }
 
@@ -281,19 +271,6 @@ struct Acc {
                 for (int b = 0; b < B; ++b)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) a[s][k][b][q] = make_float2(0.f, 0.f);
-    }
-    // the lane's raw accumulators to / from shared memory (hand-off of a split row's state):
-    // float j of lane l at base + (j*32 + l), so a warp's accesses are conflict-free
-    static constexpr int kFloats = S * N * B * 8;
-    __device__ __forceinline__ void store(float* base, int lane) const {
-        const float* f = reinterpret_cast<const float*>(a);
-#pragma unroll
-        for (int j = 0; j < kFloats; ++j) base[j * 32 + lane] = f[j];
-    }
-    __device__ __forceinline__ void load(const float* base, int lane) {
-        float* f = reinterpret_cast<float*>(a);
-#pragma unroll
-        for (int j = 0; j < kFloats; ++j) f[j] = base[j * 32 + lane];
     }
     // sum over sets of plane q, vector b (pos - neg when N == 2)
     __device__ __forceinline__ float2 total(int b, int q) const {
@@ -434,25 +411,21 @@ __device__ __forceinline__ void epilogue(const Params& p, const float* T0, int64
 
 // Shared-memory carve-up (bytes), identical on host (plan) and device.
 struct SmemLayout {
-    int64_t x_bytes, scratch_off, tot_off, scale_off, slot_off, cnt_off, bar_off, total;
+    int64_t x_bytes, scratch_off, tot_off, scale_off, bar_off, total;
 };
 // x first (1024-B aligned for the 128B-swizzled TMA boxes), then per-warp reduction scratch
 // (multi-tile path), then -- single tile only -- the reduced totals of every CTA row
-// ([rows][NV] floats), the CTA's row scales, the split-row hand-off slots (one per warp,
-// 32 lanes x the lane's accumulator floats) and their flags, and one mbarrier per x slice.
-// Single tile: x_chunks = 32*parts*J per vector; multi-tile: the tile width.
+// ([rows][NV] floats), the CTA's row scales and one mbarrier per x slice.
+// Single tile: x_chunks = 32*J per vector; multi-tile: the tile width.
 __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
-                                                  int nbars, int rows, int parts) {
+                                                  int nbars, int rows) {
     const int64_t nv = next_pow2(8 * B);
-    const int64_t acc_floats = (B <= 2 ? 2 : 1) * B * 8;  // Acc<B>::kFloats
     SmemLayout L;
     L.x_bytes = (int64_t)B * x_chunks * 128;
     L.scratch_off = L.x_bytes;
     L.tot_off = L.scratch_off + (single ? 0 : (int64_t)warps * nv * 4);
     L.scale_off = L.tot_off + (single ? (int64_t)rows * nv * 4 : 0);
-    L.slot_off = L.scale_off + (single ? 16 * (int64_t)rows : 0);
-    L.cnt_off = L.slot_off + (single && parts > 1 ? (int64_t)(warps + 1) * 32 * acc_floats * 4 : 0);
-    L.bar_off = L.cnt_off + (single ? ((int64_t)(warps + 1) * 4 + 7) / 8 * 8 : 0);
+    L.bar_off = L.scale_off + (single ? 16 * (int64_t)rows : 0);
     L.total = L.bar_off + (single ? 8 * (int64_t)nbars : 0) + 1024;  // + base alignment slack
     return L;
 }
@@ -473,9 +446,9 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     const int nwarps = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool single = p.single != 0;
-    const int nbars = single ? p.parts * p.J0 : 0;
-    const SmemLayout SL = smem_layout(B, single ? 32 * p.parts * p.J0 : p.x_stride, nwarps,
-                                      single, nbars, p.rows_cap, p.parts);
+    const int nbars = single ? p.J : 0;
+    const SmemLayout SL = smem_layout(B, single ? 32 * p.J : p.x_stride, nwarps, single, nbars,
+                                      p.rows_cap);
     float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * NV;
     const uint32_t bars = xs + (uint32_t)SL.bar_off;
 
@@ -508,79 +481,51 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     acc.zero();
 
     if (single) {
-        // Work units: row r of the CTA is split into P = p.parts (1 or 2)
-        // column parts (a function of m and B only); unit u = (row u/P, part u%P).  The
-        // CTA's NR*P units are cut into contiguous per-warp ranges whose sizes differ by at
-        // most one, the longer ones on warps 0..e-1, so the four SM sub-partitions (warp % 4)
-        // get equal work.  A row's lane accumulators run over part P-1 first, then part 0
-        // (whichever warps hold them), and the row is reduced once, after part 0: a row split
-        // at a warp boundary has its part 1 at the *start* of the next warp's range, which
-        // hands its lane state to this warp through shared memory before this warp reaches
-        // the row's part 0 at the *end* of its own range.  So a row's arithmetic depends on
-        // (m, B) only -- never on n, the shard, the grid or the warp split.
-        // Unit indices are relative to the CTA (int32: n <= 2^30, check_layer).
-        const int P = p.parts;
-        const int U = (int)(r1 - r0) * P;
-        const int ub = U / nwarps, ue = U - ub * nwarps;
-        const int u0 = warp * ub + (warp < ue ? warp : ue);
-        const int u1 = u0 + ub + (warp < ue ? 1 : 0);
-        const int len = p.split;                           // chunks per part
-        const int J = p.J0;                                // sweeps per part
-        const bool lastok = lane < len - 32 * (J - 1);     // lane active in a part's last sweep
-        // rows touched by this warp: [ra, rz]; with P == 2 the first may lack part 0 (its
-        // part 0 is the previous warp's) and the last may lack part 1 (the next warp's)
-        const int ra = u0 / P, rz = (u1 - 1) / P;
-        auto has_part = [&](int r, int h) { return r * P + h >= u0 && r * P + h < u1; };
+        // Rows: the CTA's rows are cut into contiguous per-warp ranges
+        // [w0, w1) whose sizes differ by at most one, the longer ones on warps 0..e-1, so the
+        // four SM sub-partitions (warp % 4) get equal work (+-1 row).  A row is J sweeps of 32
+        // chunks, lane = chunk within the sweep; its arithmetic depends on (m, B) only --
+        // never on n, the shard, the grid or the warp split.  Row indices are relative to
+        // the CTA (int32: n <= 2^30, check_layer).
+        const int NRc = (int)(r1 - r0);
+        const int ub = NRc / nwarps, ue = NRc - ub * nwarps;
+        const int w0 = warp * ub + (warp < ue ? warp : ue);
+        const int w1 = w0 + ub + (warp < ue ? 1 : 0);
+        const int J = p.J;
+        const bool lastok = lane < (int)p.W - 32 * (J - 1);  // lane active in the last sweep
 
         // the CTA's row scales -> shared memory (cp.async, before griddepcontrol.wait: scales
         // are weights), read by the epilogue at the end
         {
-            const int ns = p.per_row_scales ? 4 * (int)(r1 - r0) : 4;
+            const int ns = p.per_row_scales ? 4 * NRc : 4;
             const float* src = p.scales + (p.per_row_scales ? 4 * r0 : 0);
             const uint32_t dst = xs + (uint32_t)SL.scale_off;
             for (int i = threadIdx.x; i < ns; i += blockDim.x) cp_async4(dst + 4u * i, src + i);
             cp_async_wait_all();  // this thread's copies; the __syncthreads below publishes them
         }
 
-        // Weight stream (a4): the warp's units in processing order (per row: part P-1, then
-        // part 0); each lane reads its 16-byte chunk of a sweep with a streaming 128-bit load,
-        // two sweeps ahead, the first two issued before griddepcontrol.wait (weights never
-        // depend on the previous kernel).  Lanes past a part's end load zeros, so no predicate
-        // fires for them.
-        // producer position: row pr, part ph, sweep pk; pptr = this lane's chunk of the sweep
-        // (advanced incrementally: +32 chunks per sweep, one jump per part)
-        int pr = ra, ph = has_part(ra, P - 1) ? P - 1 : 0, pk = 0;
-        // sweep pk of a part is loaded iff pk < kv: kv = J on lanes active in the part's last
-        // sweep, J - 1 on the others, 0 past the warp's last row (one compare per sweep)
+        // Weight stream (a4): the warp's rows in order; each lane reads its 16-byte chunk of
+        // a sweep with a streaming 128-bit load, two sweeps ahead, the first two issued
+        // before griddepcontrol.wait (weights never depend on the previous kernel).  Lanes
+        // past the row's end load zeros, so no predicate fires for them.  Sweep pk of the
+        // producer's row pr is loaded iff pk < kv: kv = J on lanes active in the last sweep,
+        // J - 1 on the others, 0 past the warp's last row (one compare per sweep).
         const int kvl = lastok ? J : J - 1;
-        int kv = ra <= rz ? kvl : 0;
-        const uint4* pptr = p.packed + (r0 + ra) * p.W + ph * len + lane;
-        const int64_t Wl = p.W;
+        int pr = w0, pk = 0, kv = w0 < w1 ? kvl : 0;
+        const uint4* pptr = p.packed + (r0 + w0) * p.W + lane;
+        const int64_t jrow = p.W - 32 * (int64_t)J;  // from the chunk after a row to the next
         auto load_next = [&]() -> uint4 {
             const uint4 w = ldg_stream_lt(pptr, pk, kv);
             pptr += 32;
-            if (++pk == J) {  // next part: part 0 of this row, else part P-1 of the next row
+            if (++pk == J) {  // next row
                 pk = 0;
-                pptr -= 32 * J + ph * len;  // back to the start of this part's row
-                if (ph > 0 && has_part(pr, 0)) {
-                    ph = 0;
-                } else {
-                    ++pr;
-                    ph = has_part(pr, P - 1) ? P - 1 : 0;
-                    pptr += Wl;
-                    kv = pr <= rz ? kvl : 0;
-                }
-                pptr += ph * len;
+                pptr += jrow;
+                kv = ++pr < w1 ? kvl : 0;
             }
             return w;
         };
         uint4 qa = load_next(), qb = load_next();
-        // hand-off slots for split rows: slot w = lane state of the row whose part 1 starts
-        // warp w's range (NV2 floats per lane), flag[w] = 1 once written
-        float* slot = reinterpret_cast<float*>(smem + SL.slot_off);
-        int* flag = reinterpret_cast<int*>(smem + SL.cnt_off);
-        if (threadIdx.x <= nwarps) flag[threadIdx.x] = 0;
-        __syncthreads();  // mbarrier inits, flags and staged scales visible
+        __syncthreads();  // mbarrier inits and staged scales visible
         trace(tslot, 1);
 #if WW_DEBUG_FLAGS
         if (!(p.dbg & 1))
@@ -592,20 +537,18 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         } else {
             stage_x_regions_cp_async<B>(p, xs, bars);
         }
-        uint32_t seen = 0;  // bit h: the x slices of part h have been waited for
         trace(tslot, 3);
         int tr_sweep = 4;
 
         const uint32_t l7 = (uint32_t)(lane & 7) << 4;  // swizzle key of the lane's chunks
-        const uint32_t xb0 = xs + (uint32_t)lane * 128u, xpart = (uint32_t)(B * J * 4096);
+        const uint32_t xb = (xs + (uint32_t)lane * 128u) | l7;
         const uint32_t bstride = (uint32_t)J * 4096u;
         float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][NV]
-        auto sweep_part = [&](int h) {
-            if (!((seen >> h) & 1u)) {  // first unit of this part: its x slices must be in
-                for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * (h * J + j));
-                seen |= 1u << h;
-            }
-            uint32_t xc = (xb0 + (uint32_t)h * xpart) | l7;
+        if (w0 < w1)  // x slices in before the warp's first sweep
+            for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * j);
+#pragma unroll 1
+        for (int r = w0; r < w1; ++r) {
+            uint32_t xc = xb;
 #pragma unroll 1
             for (int k = 0; k < J; ++k) {
                 const uint4 cur = qa;
@@ -618,30 +561,6 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                     chunk<B>(acc, cur, xc, bstride);
                 xc += 4096u;
             }
-        };
-#pragma unroll 1
-        for (int r = ra; r <= rz; ++r) {
-            if (P > 1 && has_part(r, 1)) {
-                sweep_part(1);
-                if (!has_part(r, 0)) {  // part 0 is the previous warp's: hand the state over
-                    acc.store(slot + warp * Acc<B>::kFloats * 32, lane);
-                    __syncwarp();
-                    if (lane == 0) {
-                        __threadfence_block();
-                        *reinterpret_cast<volatile int*>(flag + warp) = 1;
-                    }
-                    acc.zero();
-                    continue;
-                }
-            } else if (P > 1) {  // part 1 was the next warp's first unit: continue its state
-                if (lane == 0)
-                    while (*reinterpret_cast<volatile int*>(flag + warp + 1) == 0) {
-                    }
-                __syncwarp();
-                __threadfence_block();
-                acc.load(slot + (warp + 1) * Acc<B>::kFloats * 32, lane);
-            }
-            sweep_part(0);
             // reduce the row over the lanes (a7) into the CTA's totals
             reduce_to<B>(acc, tot + r * NV);
             if (tr_sweep < 29) trace(tslot, tr_sweep++);
@@ -754,32 +673,22 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     // one CTA per SM (persistent), each owning a contiguous, balanced row range
     const int64_t grid = std::min<int64_t>(sms, L->n);
     const int64_t rows = (L->n + grid - 1) / grid;  // rows per CTA (at most)
-    // Single x tile: a row is split into P = 2 equal column parts of >= 64 chunks (2 sweeps)
-    // when W is even and B <= 2 (the split-row hand-off carries the lane accumulators), else
-    // P = 1; the choice depends on (m, B) only (x must fit kXBudgetBytes).
-    int parts = 1;
-    for (int cand : {2})
-        if (B <= 2 && W % cand == 0 && W / cand >= 64 &&
-            (int64_t)B * 32 * cand * ((W / cand + 31) / 32) * 128 <= kXBudgetBytes) {
-            parts = cand;
-            break;
-        }
-    const int64_t split = W / parts;
-    auto sweeps = [&](int pr, int64_t sp) { return pr * ((sp + 31) / 32); };
-    auto single_bytes = [&](int pr, int64_t sp) {  // + the CTA's row totals and scales
-        return smem_layout(B, (int)(32 * sweeps(pr, sp)), warps, true, (int)sweeps(pr, sp),
-                           (int)std::min<int64_t>(rows, 1 << 20), pr).total;
-    };
+    // Single x tile: the whole row is one work unit of T = ceil(W/32) sweeps (x must fit
+    // kXBudgetBytes); else column tiles.  (Splitting rows into column parts handed between
+    // warps measured slower once the per-sweep load logic was one compare: DESIGN.md §6.)
+    const int64_t T = (W + 31) / 32;
+    const int64_t single_bytes =  // + the CTA's row totals and scales
+        smem_layout(B, (int)(32 * T), warps, true, (int)T, (int)std::min<int64_t>(rows, 1 << 20))
+            .total;
     li->grid = (int32_t)grid;
     li->block = 32 * warps;
     li->num_sms = sms;
-    if ((int64_t)B * 32 * sweeps(parts, split) * 128 <= kXBudgetBytes &&
-        single_bytes(parts, split) <= kSmemBudget) {
+    if ((int64_t)B * 32 * T * 128 <= kXBudgetBytes && single_bytes <= kSmemBudget) {
         li->tile_chunks = (int32_t)W;
         li->tiles = 1;
-        li->parts = parts;
-        li->split_chunks = (int32_t)split;
-        li->smem_bytes = (int32_t)single_bytes(parts, split);
+        li->parts = 1;
+        li->split_chunks = (int32_t)W;
+        li->smem_bytes = (int32_t)single_bytes;
         li->path = 0;
         return WW_OK;
     }
@@ -792,7 +701,7 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     li->parts = 1;
     li->split_chunks = (int32_t)W;
     li->path = 1;
-    li->smem_bytes = (int32_t)smem_layout(B, (int)tc, warps, false, 0, 0, 1).total;
+    li->smem_bytes = (int32_t)smem_layout(B, (int)tc, warps, false, 0, 0).total;
     return WW_OK;
 }
 
@@ -938,9 +847,7 @@ ww_status launch_batch(const ww_layer* L, const void* packed_d, const float* sca
     p.conv = L->conv;
     p.tile_chunks = li.tile_chunks;
     p.ntiles = li.tiles;
-    p.parts = li.parts;
-    p.split = li.split_chunks;
-    p.J0 = (li.split_chunks + 31) / 32;
+    p.J = (int32_t)((p.W + 31) / 32);
     p.rows_cap = (int32_t)((L->n + li.grid - 1) / li.grid);
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
     p.x_stride = (li.tile_chunks + 31) / 32 * 32;

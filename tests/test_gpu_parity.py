@@ -64,6 +64,15 @@ def test_every_batch_size_and_batch_invariance(B):
         assert np.array_equal(y1[0].cpu().numpy(), yb[b])
 
 
+@pytest.mark.parametrize("m", [1537, 3000, 5504])
+def test_ragged_last_sweep_batch2(m):
+    # rows whose last 32-chunk sweep is partial (idle lanes load zeros), two vectors
+    case = LayerCase(300, m, seed=m, B=2).device(ww, torch)
+    assert (-(-m // 16)) % 32 != 0
+    for conv in CONVS:
+        assert_parity(case.gpu(ww, torch, conv), case.oracle(ORC[conv]), case)
+
+
 def test_multi_tile_long_rows():
     # x larger than one shared-memory tile (B=1: 184 KB = 23552 complex columns)
     case = LayerCase(40, 30000, seed=3).device(ww, torch)
@@ -121,11 +130,11 @@ def test_determinism_and_pdl_flag():
         assert np.array_equal(y, ys[0])
 
 
-@pytest.mark.parametrize("m", [128, 1000, 2048, 4096, 5504])
+@pytest.mark.parametrize("m", [128, 1000, 1537, 2000, 2048, 3000, 4096, 5504])
 def test_row_results_independent_of_n(m):
-    # a row's arithmetic depends on (m, B) only (ww.h ww_launch_info: column parts): the
+    # a row's arithmetic depends on (m, B) only (ww.h ww_launch_info: whole rows): the
     # first n' rows of an n-row layer, launched alone, are bitwise the same for every n'
-    # (different CTA row ranges, different per-warp unit ranges and split-row slots)
+    # (different CTA row ranges and per-warp row ranges)
     n = 1500
     case = LayerCase(n, m, seed=m + 5).device(ww, torch)
     full = case.gpu(ww, torch, ww.CONV_EQ1)[0]
