@@ -41,6 +41,7 @@ inline int warps_for_b(int B) { return B <= 4 ? 16 : 8; }
 constexpr int kXBudgetBytes = 184 * 1024;  // x tile per CTA (multi-tile path)
 constexpr int kGroup = 4;                  // batches above this run as groups of 4 vectors
 constexpr int64_t kSmemBudget = 226 * 1024; // single-tile path: all shared memory of a CTA
+constexpr int kPrefetch = 2;                 // L2 prefetch distance beyond the weight loads
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
@@ -83,6 +84,13 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// L2 prefetch of the 16-byte chunk at p when a < b (one compare + one predicated PREFETCH)
+__device__ __forceinline__ void prefetch_chunk_lt(const uint4* p, int a, int b) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %1, %2;\n\t@q prefetch.global.L2 [%0];\n\t}"
+        :: "l"(p), "r"(a), "r"(b));
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -435,7 +443,9 @@ __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps
 template <int B>
 __host__ __device__ constexpr int min_blocks() { return B == 1 ? 2 : 1; }
 
-template <int B>
+// kStream: single x tile with W a multiple of 32 -- the warp's rows are one contiguous stream
+// of whole sweeps (launch_b picks the instantiation; each has only one sweep loop)
+template <int B, bool kStream>
 __global__ void __launch_bounds__(warps_for<B>() * 32, min_blocks<B>())
 wl_gemv_kernel(const __grid_constant__ Params p) {
     constexpr int NV = next_pow2(8 * B);
@@ -514,7 +524,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         int pr = w0, pk = 0, kv = w0 < w1 ? kvl : 0;
         const uint4* pptr = p.packed + (r0 + w0) * p.W + lane;
         const int64_t jrow = p.W - 32 * (int64_t)J;  // from the chunk after a row to the next
-        auto load_next = [&]() -> uint4 {
+        auto load_rows = [&]() -> uint4 {
             const uint4 w = ldg_stream_lt(pptr, pk, kv);
             pptr += 32;
             if (++pk == J) {  // next row
@@ -524,48 +534,64 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             }
             return w;
         };
-        uint4 qa = load_next(), qb = load_next();
-        __syncthreads();  // mbarrier inits and staged scales visible
-        trace(tslot, 1);
-#if WW_DEBUG_FLAGS
-        if (!(p.dbg & 1))
-#endif
-            pdl_wait();
-        trace(tslot, 2);
-        if (p.use_tma) {
-            stage_x_regions_tma<B>(p, xs, bars);
-        } else {
-            stage_x_regions_cp_async<B>(p, xs, bars);
-        }
-        trace(tslot, 3);
-        int tr_sweep = 4;
-
-        const uint32_t l7 = (uint32_t)(lane & 7) << 4;  // swizzle key of the lane's chunks
-        const uint32_t xb = (xs + (uint32_t)lane * 128u) | l7;
-        const uint32_t bstride = (uint32_t)J * 4096u;
+        // kStream: the producer only counts sweeps (no row transitions), and prefetches into
+        // L2 the chunk kPrefetch sweeps beyond each load
+        const int nsweeps = (w1 - w0) * J;
+        auto load_stream = [&]() -> uint4 {
+            prefetch_chunk_lt(pptr + 32 * kPrefetch, pk + kPrefetch, nsweeps);
+            const uint4 w = ldg_stream_lt(pptr, pk, nsweeps);
+            pptr += 32;
+            ++pk;
+            return w;
+        };
         float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][NV]
-        if (w0 < w1)  // x slices in before the warp's first sweep
-            for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * j);
-#pragma unroll 1
-        for (int r = w0; r < w1; ++r) {
-            uint32_t xc = xb;
-#pragma unroll 1
-            for (int k = 0; k < J; ++k) {
-                const uint4 cur = qa;
-                qa = qb;
-                qb = load_next();
-                if (tr_sweep < 29) trace(tslot, tr_sweep++);
+        auto run = [&](auto&& load_next) {
+            uint4 qa = load_next(), qb = load_next();
+            __syncthreads();  // mbarrier inits and staged scales visible
+            trace(tslot, 1);
 #if WW_DEBUG_FLAGS
-                if (!(p.dbg & 2))
+            if (!(p.dbg & 1))
 #endif
-                    chunk<B>(acc, cur, xc, bstride);
-                xc += 4096u;
+                pdl_wait();
+            trace(tslot, 2);
+            if (p.use_tma) {
+                stage_x_regions_tma<B>(p, xs, bars);
+            } else {
+                stage_x_regions_cp_async<B>(p, xs, bars);
             }
-            // reduce the row over the lanes (a7) into the CTA's totals
-            reduce_to<B>(acc, tot + r * NV);
-            if (tr_sweep < 29) trace(tslot, tr_sweep++);
-            acc.zero();
-        }
+            trace(tslot, 3);
+            int tr_sweep = 4;
+
+            const uint32_t l7 = (uint32_t)(lane & 7) << 4;  // swizzle key of the lane's chunks
+            const uint32_t xb = (xs + (uint32_t)lane * 128u) | l7;
+            const uint32_t bstride = (uint32_t)J * 4096u;
+            if (w0 < w1)  // x slices in before the warp's first sweep
+                for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * j);
+#pragma unroll 1
+            for (int r = w0; r < w1; ++r) {
+                uint32_t xc = xb;
+#pragma unroll 1
+                for (int k = 0; k < J; ++k) {
+                    const uint4 cur = qa;
+                    qa = qb;
+                    qb = load_next();
+                    if (tr_sweep < 29) trace(tslot, tr_sweep++);
+#if WW_DEBUG_FLAGS
+                    if (!(p.dbg & 2))
+#endif
+                        chunk<B>(acc, cur, xc, bstride);
+                    xc += 4096u;
+                }
+                // reduce the row over the lanes (a7) into the CTA's totals
+                reduce_to<B>(acc, tot + r * NV);
+                if (tr_sweep < 29) trace(tslot, tr_sweep++);
+                acc.zero();
+            }
+        };
+        if constexpr (kStream)
+            run(load_stream);
+        else
+            run(load_rows);
         trace(tslot, 29);  // sweeps done
         // Epilogue (a8) for all rows of the CTA at once: thread t takes (row, vector) items
         // t, t + blockDim, ...: 8 scale multiplies on the row's totals, one coalesced
@@ -741,19 +767,22 @@ bool encode_x_map(Params& p, int B) {
 template <int B>
 cudaError_t launch_b(const Params& p, const ww_launch_info& li, cudaStream_t s, bool pdl) {
     static bool attr_set = false;
+    void (*const kernels[2])(Params) = {wl_gemv_kernel<B, false>, wl_gemv_kernel<B, true>};
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(wl_gemv_kernel<B>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
-        if (e != cudaSuccess) return e;
-        // always the largest shared-memory carveout: consecutive launches of different shapes
-        // then never force an L1/shared reconfiguration, and the PDL-launched next layer's CTA
-        // can co-reside with this one
-        e = cudaFuncSetAttribute(wl_gemv_kernel<B>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 (int)cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return e;
+        for (auto k : kernels) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 227 * 1024);
+            if (e != cudaSuccess) return e;
+            // always the largest shared-memory carveout: consecutive launches of different
+            // shapes then never force an L1/shared reconfiguration, and the PDL-launched next
+            // layer's CTA can co-reside with this one
+            e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
+            if (e != cudaSuccess) return e;
+        }
         attr_set = true;
     }
+    const bool stream_rows = p.single && (p.W & 31) == 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)li.grid);
     cfg.blockDim = dim3((unsigned)li.block);
@@ -764,7 +793,7 @@ cudaError_t launch_b(const Params& p, const ww_launch_info& li, cudaStream_t s, 
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, wl_gemv_kernel<B>, p);
+    return cudaLaunchKernelEx(&cfg, kernels[stream_rows ? 1 : 0], p);
 }
 
 cudaError_t launch(const Params& p, const ww_launch_info& li, int B, cudaStream_t s, bool pdl) {

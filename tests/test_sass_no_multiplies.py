@@ -15,15 +15,18 @@ LIB = os.path.join(ROOT, "paper_2604_20913_b200", "libww.so")
 FP_MUL = re.compile(r"\b(FMUL2?|FFMA2?|DMUL|DFMA|HMUL2|FMUL32I|FFMA32I)\b")
 
 
-def _kernel_sass(name_pat):
+def _kernels_sass(name_pat):
+    """SASS of every function matching name_pat (both instantiations of a batch size: row
+    stream and row-by-row producers)."""
     if not shutil.which("cuobjdump"):
         pytest.skip("cuobjdump not available")
     out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s*Function : ", out)
-    for f in funcs:
-        if re.match(name_pat, f):
-            return [ln.split(";")[0].strip() for ln in f.splitlines() if re.search(r"/\*[0-9a-f]{4}\*/", ln)]
-    pytest.fail(f"kernel {name_pat} not found in {LIB}")
+    found = [[ln.split(";")[0].strip() for ln in f.splitlines()
+              if re.search(r"/\*[0-9a-f]{4}\*/", ln)] for f in funcs if re.match(name_pat, f)]
+    if not found:
+        pytest.fail(f"kernel {name_pat} not found in {LIB}")
+    return found
 
 
 def _strip(ln):
@@ -32,7 +35,11 @@ def _strip(ln):
 
 @pytest.mark.parametrize("B", [1, 4])
 def test_accumulation_loop_has_no_fp_multiply(B):
-    sass = [_strip(l) for l in _kernel_sass(rf"_ZN\S*wl_gemv_kernelILi{B}EE")]
+    for k in _kernels_sass(rf"_ZN\S*wl_gemv_kernelILi{B}E"):
+        _check_loop(B, [_strip(l) for l in k])
+
+
+def _check_loop(B, sass):
     # accumulation blocks: maximal runs of predicated FADD2 (Eqs. 6-7 as predicated packed
     # adds) no more than 12 instructions apart -- one block per unrolled 64-code chunk body
     idx = [i for i, l in enumerate(sass) if re.match(r"@!?P\d\s+FADD2\b", l)]
@@ -52,7 +59,11 @@ def test_accumulation_loop_has_no_fp_multiply(B):
 
 
 def test_scale_multiplies_exist_only_in_epilogue():
-    sass = [_strip(l) for l in _kernel_sass(r"_ZN\S*wl_gemv_kernelILi1EE")]
+    for k in _kernels_sass(r"_ZN\S*wl_gemv_kernelILi1E"):
+        _check_epilogue([_strip(l) for l in k])
+
+
+def _check_epilogue(sass):
     fmul = [i for i, l in enumerate(sass) if re.search(r"\bFMUL\b", l)]
     fadd2 = [i for i, l in enumerate(sass) if re.match(r"@!?P\d\s+FADD2\b", l)]
     assert fmul, "the epilogue's scale multiplies (P:1002-1011) should be FMULs"
