@@ -348,7 +348,7 @@ def run_ours(args, world, rank, local):
                    "graph": graph is not None, "pdl": not args.no_pdl,
                    "l2": "inputs > L2: 1.62 GB of weights per step streamed from HBM"
                          if args.workload == "c4" else "rotating replicas >= 4x L2",
-                   "launch": ww.query_launch(ww.Layer(2048, 5504), args.batch)},
+                   "launch": _launch_configs(ww, stack, args)},
         "us_per_layer": round(1e3 * ms_step / layers_per_step, 3),
         "launches_per_step": launches_per_step,
         "per_shape_us": per_shape,
@@ -408,6 +408,17 @@ def _e2e(stack, args, s, dev, graph, world, alg_bytes):
     return {"value": round(alg_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8),
             "ms_per_step": round(ms, 4)}
+
+
+def _launch_configs(ww, stack, args):
+    """ww_query_launch of every distinct launch shape of the step (per-rank rows)."""
+    if args.workload == "c4":
+        shapes = {}
+        for st in stack.stages:
+            shapes.setdefault(f"{st.name} {st.ylocal}x{st.m}", (st.ylocal, st.m))
+    else:
+        shapes = {f"{stack.spec.name} {stack.nloc}x{stack.spec.m}": (stack.nloc, stack.spec.m)}
+    return {k: ww.query_launch(ww.Layer(max(n, 1), m), args.batch) for k, (n, m) in shapes.items()}
 
 
 class _ReplicaLayer:

@@ -584,6 +584,17 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 }
                 // reduce the row over the lanes (a7) into the CTA's totals
                 reduce_to<B>(acc, tot + r * NV);
+                // epilogue (a8) of the row by its own warp (no CTA barrier): lane b < B
+                // applies the row's 8 scale multiplies to vector b's totals, one complex64
+                // store
+                if (lane < B) {
+                    float T[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) T[i] = tot[r * NV + 8 * lane + i];
+                    const float* sr = reinterpret_cast<const float*>(smem + SL.scale_off) +
+                                      (p.per_row_scales ? 4 * r : 0);
+                    store_y(p, T, sr, lane, r0 + r);
+                }
                 if (tr_sweep < 29) trace(tslot, tr_sweep++);
                 acc.zero();
             }
@@ -593,21 +604,6 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         else
             run(load_rows);
         trace(tslot, 29);  // sweeps done
-        // Epilogue (a8) for all rows of the CTA at once: thread t takes (row, vector) items
-        // t, t + blockDim, ...: 8 scale multiplies on the row's totals, one coalesced
-        // complex64 store per item.
-        __syncthreads();
-        const int NR = (int)(r1 - r0);
-        for (int it = threadIdx.x; it < NR * B; it += blockDim.x) {
-            const int b = it / NR, lr = it - b * NR;
-            const float* T0 = tot + lr * NV + 8 * b;
-            float T[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) T[i] = T0[i];
-            const float* sr = reinterpret_cast<const float*>(smem + SL.scale_off) +
-                              (p.per_row_scales ? 4 * lr : 0);
-            store_y(p, T, sr, b, r0 + lr);
-        }
         trace(tslot, 31);
         return;
     }
