@@ -329,8 +329,10 @@ __device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xl, u
 #pragma unroll
         for (int b = 0; b < B; ++b) {  // each decoded code drives all B vectors (a9)
             const float4 v = lds128(xa + b * bstride);
-            column<N>(acc.a[0][0][b], acc.a[0][N - 1][b], bits_a, make_float2(v.x, v.y));
+            // (odd column first: the same sums -- each column-parity set keeps its own
+            // order -- but ptxas then needs no predicate spill across the R2Ps)
             column<N>(acc.a[S - 1][0][b], acc.a[S - 1][N - 1][b], bits_b, make_float2(v.z, v.w));
+            column<N>(acc.a[0][0][b], acc.a[0][N - 1][b], bits_a, make_float2(v.x, v.y));
         }
     }
 }
