@@ -4,8 +4,9 @@
 // Hot path per output row i (Alg. 1, re-designed for B200):
 //   * weights: one 16-byte COL4 chunk (16 columns x 4 planes, 2 bits per code) per lane per
 //     step, 128-bit coalesced non-allocating loads straight from HBM (a4);
-//   * activations: x staged once per CTA in shared memory with cp.async (a3; O2),
-//     16-byte granules XOR-swizzled so the 32 lanes (32 different chunks) read conflict-free;
+//   * activations: x staged once per CTA in shared memory by TMA (cp.async.bulk.tensor, else
+//     cp.async) (a3; O2), 16-byte granules XOR-swizzled (128B swizzle) so the 32
+//     lanes (32 different chunks) read conflict-free;
 //   * decode (a5; Eqs. 4-5, O1 P:1033): byte k of a chunk holds the 8 code bits of
 //     column k; each bit predicates one packed-fp32 add (FADD2) of the pair (x_re, x_im) or
 //     its negation into that plane's pair accumulator (Eqs. 6-7), so one decoded
@@ -32,7 +33,6 @@
 
 namespace {
 
-// warps per CTA: 16 while the B accumulators leave room, 8 (255-register cap) above
 // warps per CTA, a multiple of 4 so the four SM sub-partitions get equal warps: 16 while
 // the B accumulators leave room, 8 (255-register cap) above
 template <int B>
