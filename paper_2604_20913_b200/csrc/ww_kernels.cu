@@ -762,6 +762,9 @@ bool encode_x_map(Params& p, int B) {
     return r == CUDA_SUCCESS;
 }
 
+bool g_force_rows = false;  // tests: run the row-by-row instantiation where kStream applies
+int g_last_stream = -1;     // tests: 1 if the last launch ran the kStream instantiation
+
 template <int B>
 cudaError_t launch_b(const Params& p, const ww_launch_info& li, cudaStream_t s, bool pdl) {
     static bool attr_set = false;
@@ -780,7 +783,8 @@ cudaError_t launch_b(const Params& p, const ww_launch_info& li, cudaStream_t s, 
         }
         attr_set = true;
     }
-    const bool stream_rows = p.single && (p.W & 31) == 0;
+    const bool stream_rows = p.single && (p.W & 31) == 0 && !g_force_rows;
+    g_last_stream = stream_rows ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)li.grid);
     cfg.blockDim = dim3((unsigned)li.block);
@@ -831,6 +835,9 @@ ww_status check_layer(const ww_layer* L, const char* fn) {
 
 // Not part of the ABI (no declaration in ww.h): lets the tests force the cp.async staging path.
 extern "C" void ww_debug_force_cp_async(int on) { g_force_cp_async = on != 0; }
+// Not part of the ABI: tests compare the two producer instantiations (kStream / row by row).
+extern "C" void ww_debug_force_rows(int on) { g_force_rows = on != 0; }
+extern "C" int ww_debug_last_stream(void) { return g_last_stream; }
 // Not part of the ABI: overhead-measurement switches for tools/chain_time.py (Params::dbg).
 extern "C" void ww_debug_set_flags(int flags) { g_debug_flags = flags; }
 // Not part of the ABI: 1 if the last WL-GEMV launch staged x with TMA, 0 cp.async, -1 none yet.

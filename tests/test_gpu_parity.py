@@ -264,6 +264,23 @@ def test_cp_async_staging_path_matches_tma_path(n, m, B):
     assert_parity(y_cpa, case.oracle(orc.CONV_EQ1), case)
 
 
+@pytest.mark.parametrize("n,m,B", [(2048, 2048, 1), (1000, 1024, 2), (7, 512, 1), (300, 4096, 4)])
+def test_row_stream_kernel_matches_row_by_row_kernel(n, m, B):
+    # rows of whole 32-chunk sweeps run the kStream instantiation (one contiguous weight
+    # stream per warp, L2 prefetch); the row-by-row producer must give the same bits
+    case = LayerCase(n, m, seed=n + m + 7 * B, B=B).device(ww, torch)
+    y_stream = case.gpu(ww, torch, ww.CONV_ALG1)
+    assert ww._lib.ww_debug_last_stream() == 1
+    ww._lib.ww_debug_force_rows(1)
+    try:
+        y_rows = case.gpu(ww, torch, ww.CONV_ALG1)
+        assert ww._lib.ww_debug_last_stream() == 0
+    finally:
+        ww._lib.ww_debug_force_rows(0)
+    assert np.array_equal(y_stream, y_rows)
+    assert_parity(y_stream, case.oracle(orc.CONV_ALG1), case)
+
+
 @pytest.mark.parametrize("n,m", [(2048, 2048), (2048, 5504), (300, 517), (1, 16)])
 @pytest.mark.parametrize("conv", CONVS)
 def test_unfused_ablation_matches_oracle(n, m, conv):
