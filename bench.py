@@ -131,41 +131,96 @@ def oracle_sample(layers=(0,), seed=0, rows=None):
     return work
 
 
-def oracle_time(work):
+def oracle_time(work, omp=False):
+    """One pass of the C fp64 oracle over the sample, in its two phases:
+    (a) unpack + build the dense complex rows, (b) evaluate Eq. 1.  Returns
+    (unpack_s, eval_s, packed_bytes)."""
     import oracle as orc
-    t = time.perf_counter()
+    tu = te = 0.0
     nbytes = 0
     for planar, nr, m, sc, x in work:
-        orc.wl_direct(planar, nr, m, sc, x, orc.CONV_EQ1)
+        t0 = time.perf_counter()
+        U, Wd = orc.build_dense(planar, nr, m, sc, omp=omp)
+        t1 = time.perf_counter()
+        orc.eval_dense(U, Wd, x, orc.CONV_EQ1, omp=omp)
+        t2 = time.perf_counter()
+        del U, Wd
+        tu += t1 - t0
+        te += t2 - t1
         nbytes += 16 * nr * ((m + 15) // 16)
-    return time.perf_counter() - t, nbytes
+    return tu, te, nbytes
+
+
+def host_info() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "nproc": usable, "cpu_count": os.cpu_count()}
+
+
+SAMPLE = ("decoder layer 0 of config 4 (q,k,v,o 2048x2048; gate,up 5504x2048; down 2048x5504), "
+          "all rows, B=1, EQ1: the C fp64 oracle's unpack + dense build, then direct evaluation")
+
+
+def cpu_baseline(seed=0, runs=3) -> dict:
+    """The oracle as it stands on this host's cores (rank 0, N = 1): median of `runs` passes
+    over decoder layer 0, single-threaded and with OpenMP over rows on every usable core,
+    unpack timed apart from evaluate.  GB/s of packed weights."""
+    import oracle as orc
+    work = oracle_sample(layers=(0,), seed=seed)
+    out = {}
+    for omp in (False, True):
+        ts = [oracle_time(work, omp) for _ in range(runs)]
+        tu = float(np.median([t[0] for t in ts]))
+        te = float(np.median([t[1] for t in ts]))
+        tt = float(np.median([t[0] + t[1] for t in ts]))
+        nb = ts[0][2]
+        out["omp" if omp else "single"] = {
+            "value": round(nb / tt / 1e9, 6), "cores": orc.num_threads(omp),
+            "unpack_s": round(tu, 4), "eval_s": round(te, 4), "total_s": round(tt, 4)}
+    allc = out["omp"]
+    return {"value": allc["value"], "unit": "GB/s", "cores": allc["cores"], "kind": "oracle",
+            "sample": SAMPLE + f"; median of {runs} runs; value = OpenMP over rows on all "
+                      "usable cores (`single` = one thread)",
+            "single_thread": out["single"], "all_cores": allc, **host_info()}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the C fp64 oracle as it stands, on the host cores (rank 0 only)."""
+    """--impl reference: the C fp64 oracle as it stands, on the host cores (rank 0 only), OpenMP
+    over rows on every usable core; one step = decoder layer 0 of config 4."""
     if rank != 0:
         return
+    import oracle as orc
     work = oracle_sample(layers=(0,), seed=args.seed)
     for _ in range(args.warmup):
-        oracle_time(work)
+        oracle_time(work, omp=True)
     ts, nb = [], 0
     for _ in range(args.steps):
-        dt, nb = oracle_time(work)
-        ts.append(dt)
+        tu, te, nb = oracle_time(work, omp=True)
+        ts.append(tu + te)
     t = float(np.sum(ts))
     value = nb * args.steps / t / 1e9
-    sample = ("decoder layer 0 of config 4 (q,k,v,o 2048x2048; gate,up 5504x2048; down "
-              "2048x5504), all rows, B=1, EQ1, orc_wl_direct (unpack to dense fp64 complex + "
-              "direct evaluation) per step")
+    cores = orc.num_threads(True)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "c4_llama2_7b_wl_decode_stack (oracle sample)", "batch": 1,
-                   "sample": sample},
-        "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": sample},
+                   "sample": SAMPLE},
+        "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": cores,
+                         "kind": "oracle", "sample": SAMPLE + "; OpenMP over rows",
+                         **host_info()},
         "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -269,6 +324,7 @@ def run_ours(args, world, rank, local):
     # ---------------- per-shape kernel time: a CUDA graph of the same projection of every
     # layer (distinct weights, so HBM-cold), CUDA events on the launching stream
     per_shape = {}
+    allgather_us = {}
     kern_ms_total = 0.0
     if args.workload == "c4":
         kinds = {}
@@ -299,6 +355,8 @@ def run_ours(args, world, rank, local):
                 kern_ms_total += per_shape[label] * 1e-3 * len(idx)
             except Exception as e:  # pragma: no cover
                 per_shape[label] = f"unavailable: {e!r}"
+            if world > 1:  # the same stages' all-gathers alone (SURVEY §8e breakdown)
+                allgather_us[label] = _time_allgathers(stack, idx, s, dev)
 
     # ---------------- e2e: host activations in, result out, through the same API calls
     e2e = _e2e(stack, args, s, dev, graph, world, alg_bytes)
@@ -333,11 +391,7 @@ def run_ours(args, world, rank, local):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        work = oracle_sample(layers=(0,), seed=args.seed)
-        dt, nb = oracle_time(work)
-        cpu = {"value": round(nb / dt / 1e9, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": "decoder layer 0 of config 4 (7 projections, all rows, B=1, EQ1), "
-                         f"{nb} packed bytes in {dt:.2f} s, single-threaded C fp64 oracle"}
+        cpu = cpu_baseline(args.seed)
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -346,14 +400,18 @@ def run_ours(args, world, rank, local):
         "config": {"workload": workload, "batch": args.batch, "layers_per_step": layers_per_step,
                    "parallelism": f"rows/{world} + NCCL all-gather" if world > 1 else "1 GPU",
                    "graph": graph is not None, "pdl": not args.no_pdl,
+                   "nccl_in_graph": bool(graph is not None and world > 1),
                    "l2": "inputs > L2: 1.62 GB of weights per step streamed from HBM"
                          if args.workload == "c4" else "rotating replicas >= 4x L2",
                    "launch": _launch_configs(ww, stack, args)},
         "us_per_layer": round(1e3 * ms_step / layers_per_step, 3),
         "launches_per_step": launches_per_step,
         "per_shape_us": per_shape,
+        "per_shape_allgather_us": allgather_us if world > 1 else None,
         "pct_of_hbm_peak": round(100 * (pa_bytes / (ms_step * 1e-3) / 1e9) / world
                                  / peaks.get("hbm_gbs", 6650.0), 2),
+        "hbm_frac": roof["hbm"]["frac"],
+        "alu_frac": roof["frac"],
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -361,6 +419,40 @@ def run_ours(args, world, rank, local):
         "clocks": clk,
     }
     print(json.dumps(out), flush=True)
+
+
+def _time_allgathers(stack, idx, s, dev, reps=5):
+    """us per all-gather of the listed stages alone (NCCL, in a CUDA graph when capture works,
+    else eager), CUDA events on the launching stream, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    def run():
+        for i in idx:
+            stack.exchange(i)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    g = None
+    try:
+        with torch.cuda.stream(s):
+            run()
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            run()
+    except Exception:
+        g = None
+        torch.cuda.synchronize(dev)
+    dist.barrier()
+    with torch.cuda.stream(s):
+        a.record(s)
+        for _ in range(reps):
+            g.replay() if g is not None else run()
+        b.record(s)
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([a.elapsed_time(b) * 1e3 / (reps * len(idx))], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"us": round(float(t.item()), 3), "graph": g is not None}
 
 
 def _ncu_traffic():
@@ -474,6 +566,34 @@ class _ReplicaLayer:
         return self.R * 8 * self.nloc * self.spec.m * self.B
 
 
+def launch_plan(gpus: int, env) -> tuple:
+    """How to honour --gpus N: ("run", world) in this process (WORLD_SIZE already set by
+    torchrun, or N = 1), ("spawn", N) to relaunch under torch.distributed.run with N ranks,
+    or ("error", why) when --gpus disagrees with an existing WORLD_SIZE."""
+    if gpus < 1:
+        return ("error", f"--gpus {gpus} < 1")
+    ws = env.get("WORLD_SIZE")
+    if ws is None:
+        return ("run", 1) if gpus == 1 else ("spawn", gpus)
+    if int(ws) != gpus:
+        return ("error", f"--gpus {gpus} but WORLD_SIZE={ws} (launch N ranks for --gpus N)")
+    return ("run", int(ws))
+
+
+def spawn_cmd(nproc: int, argv, port: int) -> list:
+    """torchrun command line that relaunches this script with nproc ranks on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -492,6 +612,18 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3
+    kind, what = launch_plan(args.gpus, os.environ)
+    if kind == "error":
+        print(f"bench.py: {what}", file=sys.stderr)
+        sys.exit(2)
+    if kind == "spawn":
+        if args.impl == "ours":
+            import torch
+            if torch.cuda.device_count() < what:
+                print(f"bench.py: --gpus {what} but only {torch.cuda.device_count()} visible "
+                      "CUDA devices", file=sys.stderr)
+                sys.exit(2)
+        sys.exit(subprocess.call(spawn_cmd(what, sys.argv[1:], _free_port())))
     if args.impl == "reference":
         # the oracle runs on rank 0's host cores; other ranks exit 0 without work
         run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))

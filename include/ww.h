@@ -64,8 +64,10 @@ typedef enum { WW_SCALES_PER_TENSOR = 0, WW_SCALES_PER_ROW = 1 } ww_scale_mode;
 
 /* launch flags (ww_layer.flags) */
 #define WW_FLAG_PDL 1u /* programmatic dependent launch: the kernel starts streaming its
-                          weights while the previous kernel on the stream finishes, and
-                          waits (griddepcontrol.wait) before touching x, y or scales */
+                          packed weights while the previous kernel on the stream finishes
+                          (so that kernel must not write the packed weights), and waits
+                          (griddepcontrol.wait) before touching x, y or the scales, which the
+                          previous kernel may therefore produce */
 
 #define WW_MAX_BATCH 16
 
@@ -120,7 +122,11 @@ ww_status ww_wl_gemv_batched(const ww_layer* L, const void* packed_d, const floa
                              const float* X_d, int64_t ldx, float* Y_d, int64_t ldy, int32_t B,
                              void* stream);
 
-/* Row sharding over `world` GPUs (ceil blocks so an all-gather has equal counts):
+/* Row sharding over `world` GPUs: the row-range parallelism of the paper's kernel
+ * (contiguous per-thread row ranges) lifted to GPUs, and SPEC's partition_rows
+ * (disjoint contiguous ranges covering all rows).  Errors: world < 1, rank not in
+ * [0, world), n < 1 or m < 1 -> WW_ERR_INVALID_ARGUMENT (out untouched).  Pure host function.
+ * Ceil blocks so an all-gather has equal counts:
  * rows_per_rank = ceil(n/world), n_padded = world*rows_per_rank, rank r owns rows
  * [r*rpr, min((r+1)*rpr, n)) (possibly empty).  Its COL4/PLANAR-row weights are the
  * contiguous byte range [packed_offset_bytes, +packed_bytes) of a COL4 buffer, its

@@ -13,7 +13,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_OMP_PATH = os.path.join(_HERE, "liboracle_omp.so")  # same source, OpenMP over rows
 _lib = None
+_libs = {}
 
 CONV_EQ1, CONV_ALG1 = 0, 1
 SCALES_PER_TENSOR, SCALES_PER_ROW = 0, 1
@@ -23,12 +25,14 @@ class OracleError(RuntimeError):
     pass
 
 
-def lib():
+def lib(omp: bool = False):
+    """The single-threaded oracle, or (omp=True) the same source built with OpenMP."""
     global _lib
-    if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            raise OracleError(f"{_LIB_PATH} missing: run __graft_entry__.build()")
-        L = ctypes.CDLL(_LIB_PATH)
+    path = _OMP_PATH if omp else _LIB_PATH
+    if path not in _libs:
+        if not os.path.exists(path):
+            raise OracleError(f"{path} missing: run __graft_entry__.build()")
+        L = ctypes.CDLL(path)
         i64, vp = ctypes.c_int64, ctypes.c_void_p
         L.orc_words_per_row.restype = i64
         L.orc_words_per_row.argtypes = [i64]
@@ -48,8 +52,16 @@ def lib():
             f.argtypes = [vp, i64, i64, vp, ctypes.c_int, ctypes.c_int, vp, i64, vp, i64, vp]
         L.orc_wl_alg1.restype = ctypes.c_int
         L.orc_wl_alg1.argtypes = [vp, i64, i64, vp, ctypes.c_int, vp, vp, i64, vp, vp]
-        _lib = L
-    return _lib
+        L.orc_build_dense.restype = ctypes.c_int
+        L.orc_build_dense.argtypes = [vp, i64, i64, vp, ctypes.c_int, vp, i64, vp, vp]
+        L.orc_eval_dense.restype = ctypes.c_int
+        L.orc_eval_dense.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp]
+        L.orc_num_threads.restype = ctypes.c_int
+        L.orc_num_threads.argtypes = []
+        _libs[path] = L
+        if not omp:
+            _lib = L
+    return _libs[path]
 
 
 def _check(rc: int, what: str):
@@ -135,6 +147,41 @@ def wl_direct(planar, n, m, scales, x, conv=CONV_EQ1, rows=None) -> np.ndarray:
 
 def wl_embedding(planar, n, m, scales, x, conv=CONV_EQ1, rows=None) -> np.ndarray:
     return _eval(lib().orc_wl_embedding, planar, n, m, scales, conv, x, rows)
+
+
+def num_threads(omp: bool = False) -> int:
+    return int(lib(omp).orc_num_threads())
+
+
+def build_dense(planar, n, m, scales, rows=None, omp=False):
+    """Phase (a): unpack + dense complex rows of U and W, each (nrows, m) complex128."""
+    planar = np.ascontiguousarray(planar, dtype=np.uint32)
+    assert planar.size == 4 * n * words_per_row(m)
+    sc = np.ascontiguousarray(scales, dtype=np.float32)
+    mode = SCALES_PER_ROW if sc.ndim == 2 else SCALES_PER_TENSOR
+    if rows is None:
+        rp, nrows = None, n
+    else:
+        rows_arr = np.ascontiguousarray(rows, dtype=np.int64)
+        rp, nrows = rows_arr.ctypes.data, rows_arr.size
+    U = np.empty((nrows, m), dtype=np.complex128)
+    Wd = np.empty((nrows, m), dtype=np.complex128)
+    _check(lib(omp).orc_build_dense(planar.ctypes.data, n, m, sc.ctypes.data, mode, rp, nrows,
+                                    U.ctypes.data, Wd.ctypes.data), "build_dense")
+    return U, Wd
+
+
+def eval_dense(U, Wd, x, conv=CONV_EQ1, omp=False):
+    """Phase (b): (B, nrows) complex128 from dense rows (bitwise == wl_direct)."""
+    nrows, m = U.shape
+    xx = np.ascontiguousarray(x, dtype=np.complex64)
+    if xx.ndim == 1:
+        xx = xx[None, :]
+    B = xx.shape[0]
+    y = np.zeros((B, nrows), dtype=np.complex128)
+    _check(lib(omp).orc_eval_dense(U.ctypes.data, Wd.ctypes.data, nrows, m, conv, xx.ctypes.data,
+                                   B, y.ctypes.data), "eval_dense")
+    return y
 
 
 def wl_alg1(planar, n, m, scales, x, rows=None):

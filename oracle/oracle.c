@@ -5,6 +5,9 @@
 #include <complex.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 int64_t orc_words_per_row(int64_t m) { return (m + 15) / 16; }
 
@@ -54,7 +57,7 @@ void orc_decode_masks(uint32_t p, uint32_t* k_pos, uint32_t* k_neg) {
 }
 
 int orc_pack_plane(const int8_t* dense, int64_t n, int64_t m, int64_t ld, uint32_t* words) {
-    if (n < 0 || m < 0 || ld < m || (!dense && n * m) || (!words && n * m)) return -1;
+    if (n < 0 || m < 0 || ld < m || (!dense && n * m != 0) || (!words && n * m != 0)) return -1;
     const int64_t W = orc_words_per_row(m);
     for (int64_t i = 0; i < n; ++i) {
         for (int64_t c = 0; c < W; ++c) {
@@ -277,4 +280,78 @@ int orc_wl_alg1(const uint32_t* planar, int64_t n, int64_t m, const float* scale
     }
     free(xre), free(xim);
     return 0;
+}
+
+/* ---- Dense two-phase form of orc_wl_direct, for timing the CPU baseline's phases
+ * separately ((a) unpack + build dense, (b) evaluate).  Same arithmetic, same
+ * order as orc_wl_direct.  Rows are independent, so an OpenMP build (-fopenmp,
+ * liboracle_omp.so) splits them over threads; results do not depend on the thread count. */
+
+int orc_build_dense(const uint32_t* planar, int64_t n, int64_t m, const float* scales,
+                    int scale_mode, const int64_t* rows, int64_t nrows, double* U, double* Wd) {
+    if (!planar || !scales || !U || !Wd || n < 1 || m < 1 || nrows < 0) return -1;
+    if (scale_mode != ORC_SCALES_PER_ROW && scale_mode != ORC_SCALES_PER_TENSOR) return -1;
+    for (int64_t r = 0; r < nrows; ++r) {
+        int64_t i = rows ? rows[r] : r;
+        if (i < 0 || i >= n) return -1;
+    }
+    int rc = 0;
+#pragma omp parallel for schedule(static) reduction(min : rc)
+    for (int64_t r = 0; r < nrows; ++r) {
+        const int64_t i = rows ? rows[r] : r;
+        int8_t* t = (int8_t*)malloc((size_t)(4 * m));
+        if (!t) {
+            rc = -3;
+            continue;
+        }
+        const int ur = unpack_row(planar, n, m, i, t);
+        if (ur != 0) {
+            rc = ur < rc ? ur : rc;
+            free(t);
+            continue;
+        }
+        double s[4];
+        row_scales(scales, scale_mode, i, s);
+        double complex* Ur = (double complex*)(U + 2 * m * r);
+        double complex* Wr = (double complex*)(Wd + 2 * m * r);
+        for (int64_t j = 0; j < m; ++j) {
+            Ur[j] = s[0] * t[0 * m + j] + I * (s[1] * t[1 * m + j]);
+            Wr[j] = s[2] * t[2 * m + j] + I * (s[3] * t[3 * m + j]);
+        }
+        free(t);
+    }
+    return rc;
+}
+
+int orc_eval_dense(const double* U, const double* Wd, int64_t nrows, int64_t m, int conv,
+                   const float* x, int64_t B, double* y) {
+    if (!U || !Wd || !x || !y || nrows < 0 || m < 1 || B < 1) return -1;
+    if (conv != ORC_CONV_EQ1 && conv != ORC_CONV_ALG1) return -1;
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < nrows; ++r) {
+        const double complex* Ur = (const double complex*)(U + 2 * m * r);
+        const double complex* Wr = (const double complex*)(Wd + 2 * m * r);
+        for (int64_t b = 0; b < B; ++b) {
+            const float* xb = x + 2 * m * b;
+            double complex acc = 0;
+            for (int64_t j = 0; j < m; ++j) { /* left to right */
+                double complex xj = (double)xb[2 * j] + I * (double)xb[2 * j + 1];
+                if (conv == ORC_CONV_EQ1)
+                    acc += Ur[j] * xj + Wr[j] * conj(xj); /* Eq. 1 */
+                else
+                    acc += (Ur[j] + conj(Wr[j])) * xj;    /* Eqs. 2-3 */
+            }
+            y[2 * (b * nrows + r)] = creal(acc);
+            y[2 * (b * nrows + r) + 1] = cimag(acc);
+        }
+    }
+    return 0;
+}
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
 }

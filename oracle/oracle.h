@@ -74,6 +74,19 @@ int orc_wl_alg1(const uint32_t* planar, int64_t n, int64_t m, const float* scale
                 int scale_mode, const float* x, const int64_t* rows, int64_t nrows, double* y,
                 int64_t counts[5]);
 
+/* The same map as orc_wl_direct in two phases (for timing them separately):
+ * orc_build_dense unpacks the listed rows and builds the dense complex rows of U and W
+ * as nrows x m complex128 (re,im interleaved) in U and Wd; orc_eval_dense
+ * evaluates Eq. 1 (EQ1) or Eqs. 2-3 (ALG1) on them, left to right -- bitwise the result of
+ * orc_wl_direct.  Rows are independent: liboracle_omp.so (built with -fopenmp) splits them
+ * over threads, with results independent of the thread count. */
+int orc_build_dense(const uint32_t* planar, int64_t n, int64_t m, const float* scales,
+                    int scale_mode, const int64_t* rows, int64_t nrows, double* U, double* Wd);
+int orc_eval_dense(const double* U, const double* Wd, int64_t nrows, int64_t m, int conv,
+                   const float* x, int64_t B, double* y);
+/* threads the library will use (1 unless built with OpenMP) */
+int orc_num_threads(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -180,11 +180,38 @@ def pack_ternary_device(planes, bad=None, stream=None, out=None):
     return out
 
 
+def _check_args(layer: Layer, packed, scales, X, Y, B: int):
+    """Marshalling checks the C ABI cannot make on raw pointers: devices, dtypes, inner
+    strides and buffer sizes (a view such as Z[:, ::2] or a complex128 tensor would
+    otherwise pass the C-side checks and give silently wrong results)."""
+    import torch
+    for name, t in (("packed", packed), ("scales", scales), ("x", X), ("y", Y)):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise TypeError(f"{name} must be a CUDA tensor")
+    for name, t in (("x", X), ("y", Y)):
+        if t.dtype != torch.complex64:
+            raise TypeError(f"{name} must be complex64 (got {t.dtype})")
+        if t.stride(-1) != 1:
+            raise ValueError(f"{name} must have unit inner stride (got {t.stride()})")
+    if X.shape[-1] != layer.m or Y.shape[-1] < layer.n:
+        raise ValueError(f"x has {X.shape[-1]} columns (m={layer.m}), y {Y.shape[-1]} (n={layer.n})")
+    if B > 1 and (X.shape[0] < B or Y.shape[0] < B):
+        raise ValueError(f"batch {B} but x {tuple(X.shape)}, y {tuple(Y.shape)}")
+    if scales.dtype != torch.float32 or not scales.is_contiguous():
+        raise TypeError("scales must be a contiguous float32 tensor")
+    need = 4 * layer.n if layer.scale_mode == SCALES_PER_ROW else 4
+    if scales.numel() < need:
+        raise ValueError(f"scales has {scales.numel()} floats, needs {need}")
+    if not packed.is_contiguous() or packed.numel() * packed.element_size() < packed_bytes(layer.n, layer.m):
+        raise ValueError(f"packed must be contiguous with >= {packed_bytes(layer.n, layer.m)} bytes")
+
+
 def wl_gemv(layer: Layer, packed, scales, x, y=None, stream=None):
     """y = WL-GEMV(x) for one complex64 CUDA vector x of length m."""
     import torch
     if y is None:
         y = torch.empty(layer.n, dtype=torch.complex64, device=x.device)
+    _check_args(layer, packed, scales, x, y, 1)
     L = layer.c()
     _check(_lib.ww_wl_gemv(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(), x.data_ptr(),
                            y.data_ptr(), _stream_ptr(stream)))
@@ -205,6 +232,9 @@ def wl_gemv_batched(layer: Layer, packed, scales, X, Y=None, stream=None):
     B = X.shape[0]
     if Y is None:
         Y = torch.empty((B, layer.n), dtype=torch.complex64, device=X.device)
+    if X.dim() != 2 or Y.dim() != 2:
+        raise ValueError("X and Y must be 2-D (B, m) / (B, n) tensors")
+    _check_args(layer, packed, scales, X, Y, B)
     L = layer.c()
     _check(_lib.ww_wl_gemv_batched(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(),
                                    X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0), B,

@@ -9,4 +9,8 @@ namespace ww {
 inline int64_t words_per_row(int64_t m) { return (m + 15) / 16; }  // 16 codes per word
 ww_status fail(ww_status s, const char* fmt, ...);                  // sets ww_last_error()
 ww_status ok();
+// per-device launch state (ww_device.cu; cached per device, mutex-guarded)
+int current_device();
+int device_sms();                                          // SM count of the current device
+int prepare_kernel(const void* fn, int max_dynamic_smem);  // cudaError_t of the attribute calls
 }  // namespace ww

@@ -21,6 +21,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 
@@ -435,7 +436,8 @@ __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps
     L.scratch_off = L.x_bytes;
     L.tot_off = L.scratch_off + (single ? 0 : (int64_t)warps * nv * 4);
     L.scale_off = L.tot_off + (single ? (int64_t)rows * nv * 4 : 0);
-    L.bar_off = L.scale_off + (single ? 16 * (int64_t)rows : 0);
+    // scales: one 16-B slot per CTA row (per-row mode) or per warp (per-tensor mode)
+    L.bar_off = L.scale_off + (single ? 16 * (int64_t)(rows > warps ? rows : warps) : 0);
     L.total = L.bar_off + (single ? 8 * (int64_t)nbars : 0) + 1024;  // + base alignment slack
     return L;
 }
@@ -506,16 +508,6 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         const int J = p.J;
         const bool lastok = lane < (int)p.W - 32 * (J - 1);  // lane active in the last sweep
 
-        // the CTA's row scales -> shared memory (cp.async, before griddepcontrol.wait: scales
-        // are weights), read by the epilogue at the end
-        {
-            const int ns = p.per_row_scales ? 4 * NRc : 4;
-            const float* src = p.scales + (p.per_row_scales ? 4 * r0 : 0);
-            const uint32_t dst = xs + (uint32_t)SL.scale_off;
-            for (int i = threadIdx.x; i < ns; i += blockDim.x) cp_async4(dst + 4u * i, src + i);
-            cp_async_wait_all();  // this thread's copies; the __syncthreads below publishes them
-        }
-
         // Weight stream (a4): the warp's rows in order; each lane reads its 16-byte chunk of
         // a sweep with a streaming 128-bit load, two sweeps ahead, the first two issued
         // before griddepcontrol.wait (weights never depend on the previous kernel).  Lanes
@@ -549,13 +541,27 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][NV]
         auto run = [&](auto&& load_next) {
             uint4 qa = load_next(), qb = load_next();
-            __syncthreads();  // mbarrier inits and staged scales visible
+            __syncthreads();  // mbarrier inits visible
             trace(tslot, 1);
 #if WW_DEBUG_FLAGS
             if (!(p.dbg & 1))
 #endif
                 pdl_wait();
             trace(tslot, 2);
+            // the warp's row scales -> shared memory (cp.async), after griddepcontrol.wait so
+            // a preceding kernel may write them (ww.h WW_FLAG_PDL); per-row mode: rows
+            // [w0, w1) at slot r, per-tensor mode: the 4 scales at the warp's own slot.  The
+            // warp waits for its copies before its first epilogue (no CTA barrier).
+            {
+                const uint32_t sdst = xs + (uint32_t)SL.scale_off;
+                if (p.per_row_scales) {
+                    const float* src = p.scales + 4 * (r0 + w0);
+                    const int ns = 4 * (w1 - w0);
+                    for (int i = lane; i < ns; i += 32) cp_async4(sdst + 16u * w0 + 4u * i, src + i);
+                } else if (lane < 4) {
+                    cp_async4(sdst + 16u * warp + 4u * lane, p.scales + lane);
+                }
+            }
             if (p.use_tma) {
                 stage_x_regions_tma<B>(p, xs, bars);
             } else {
@@ -586,6 +592,10 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 }
                 // reduce the row over the lanes (a7) into the CTA's totals
                 reduce_to<B>(acc, tot + r * NV);
+                if (r == w0) {  // before the warp's first epilogue: its scale copies have landed
+                    cp_async_wait_all();
+                    __syncwarp();
+                }
                 // epilogue (a8) of the row by its own warp (no CTA barrier): lane b < B
                 // applies the row's 8 scale multiplies to vector b's totals, one complex64
                 // store
@@ -594,7 +604,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) T[i] = tot[r * NV + 8 * lane + i];
                     const float* sr = reinterpret_cast<const float*>(smem + SL.scale_off) +
-                                      (p.per_row_scales ? 4 * r : 0);
+                                      4 * (p.per_row_scales ? r : warp);
                     store_y(p, T, sr, lane, r0 + r);
                 }
                 if (tr_sweep < 29) trace(tslot, tr_sweep++);
@@ -658,38 +668,30 @@ __global__ void pack_col4_kernel(const int8_t* __restrict__ planes, int64_t n, i
         const int64_t c = rem >> 2;
         const int q = (int)(rem & 3);
         uint32_t word = 0;
-        bool badv = false;
+        bool bad_word = false;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int64_t j = 16 * c + 4 * q + k;
             if (j >= m) continue;
             uint32_t byte = 0;
+            bool bad_col = false;  // only this column packs as zero (ww.h)
 #pragma unroll
             for (int pl = 0; pl < 4; ++pl) {
                 const int8_t t = planes[(int64_t)pl * n * ld + i * ld + j];
                 if (t == 1) byte |= 2u << (2 * pl);
                 else if (t == -1) byte |= 1u << (2 * pl);
-                else if (t != 0) badv = true;
+                else if (t != 0) bad_col = true;
             }
-            if (!badv) word |= byte << (8 * k);
+            if (!bad_col) word |= byte << (8 * k);
+            bad_word |= bad_col;
         }
         out[e] = word;
-        if (badv && bad) atomicOr(bad, 1);
+        if (bad_word && bad) atomicOr(bad, 1);
     }
 }
 
 // ------------------------------------------------------------------ launch configuration
-int num_sms() {
-    static int cached = 0;
-    if (!cached) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-            cached <= 0)
-            cached = 148;  // B200
-    }
-    return cached;
-}
+int num_sms() { return ww::device_sms(); }
 
 ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     const int64_t W = ww::words_per_row(L->m);
@@ -731,17 +733,16 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    // the driver entry point is process-wide (not per device); resolved once, thread-safe
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
         void* ptr = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
                 cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        return nullptr;
+    }();
     return fn;
 }
 
@@ -762,26 +763,15 @@ bool encode_x_map(Params& p, int B) {
     return r == CUDA_SUCCESS;
 }
 
-bool g_force_rows = false;  // tests: run the row-by-row instantiation where kStream applies
-int g_last_stream = -1;     // tests: 1 if the last launch ran the kStream instantiation
+std::atomic<bool> g_force_rows{false};  // tests: run the row-by-row instantiation where kStream applies
+std::atomic<int> g_last_stream{-1};     // tests: 1 if the last launch ran the kStream instantiation
 
 template <int B>
 cudaError_t launch_b(const Params& p, const ww_launch_info& li, cudaStream_t s, bool pdl) {
-    static bool attr_set = false;
     void (*const kernels[2])(Params) = {wl_gemv_kernel<B, false>, wl_gemv_kernel<B, true>};
-    if (!attr_set) {
-        for (auto k : kernels) {
-            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 227 * 1024);
-            if (e != cudaSuccess) return e;
-            // always the largest shared-memory carveout: consecutive launches of different
-            // shapes then never force an L1/shared reconfiguration, and the PDL-launched next
-            // layer's CTA can co-reside with this one
-            e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     (int)cudaSharedmemCarveoutMaxShared);
-            if (e != cudaSuccess) return e;
-        }
-        attr_set = true;
+    for (auto k : kernels) {  // once per (device, kernel): ww_device.cu
+        const int e = ww::prepare_kernel(reinterpret_cast<const void*>(k), 227 * 1024);
+        if (e) return (cudaError_t)e;
     }
     const bool stream_rows = p.single && (p.W & 31) == 0 && !g_force_rows;
     g_last_stream = stream_rows ? 1 : 0;
@@ -810,9 +800,9 @@ cudaError_t launch(const Params& p, const ww_launch_info& li, int B, cudaStream_
     return cudaErrorInvalidValue;
 }
 
-bool g_force_cp_async = false;  // tests: exercise the per-thread cp.async staging path
-int g_debug_flags = 0;           // tools/chain_time.py: Params::dbg
-int g_last_use_tma = -1;         // tests: whether the last launch staged x with TMA
+std::atomic<bool> g_force_cp_async{false};  // tests: exercise the per-thread cp.async staging path
+std::atomic<int> g_debug_flags{0};           // tools/chain_time.py: Params::dbg
+std::atomic<int> g_last_use_tma{-1};         // tests: whether the last launch staged x with TMA
 
 ww_status check_layer(const ww_layer* L, const char* fn) {
     if (!L) return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: null layer", fn);
@@ -833,7 +823,8 @@ ww_status check_layer(const ww_layer* L, const char* fn) {
 
 }  // namespace
 
-// Not part of the ABI (no declaration in ww.h): lets the tests force the cp.async staging path.
+// Debug hooks: not part of the ABI (no declaration in ww.h), inert unless a test or tool
+// calls them (process-wide atomics).  Lets the tests force the cp.async staging path.
 extern "C" void ww_debug_force_cp_async(int on) { g_force_cp_async = on != 0; }
 // Not part of the ABI: tests compare the two producer instantiations (kStream / row by row).
 extern "C" void ww_debug_force_rows(int on) { g_force_rows = on != 0; }

@@ -223,9 +223,21 @@ def test_argument_errors_before_launch():
     case = LayerCase(8, 32, seed=1).device(ww, torch)
     L = case.layer(ww, ww.CONV_EQ1)
     y = torch.empty(8, dtype=torch.complex64, device="cuda")
+    buf = torch.zeros(case.packed_d.numel() + 16, dtype=torch.uint8, device="cuda")
+    buf[1:1 + case.packed_d.numel()] = case.packed_d
     with pytest.raises(ww.WWError) as e:
-        ww.wl_gemv(L, case.packed_d[1:], case.scales_d, case.x_d[0], y)
+        ww.wl_gemv(L, buf[1:1 + case.packed_d.numel()], case.scales_d, case.x_d[0], y)
     assert e.value.status == ww.ERR_MISALIGNED
+    # marshalling checks in the binding: wrong dtype, inner stride, sizes
+    with pytest.raises(TypeError):
+        ww.wl_gemv(L, case.packed_d, case.scales_d, case.x_d[0].to(torch.complex128), y)
+    Z = torch.zeros((2, 64), dtype=torch.complex64, device="cuda")
+    with pytest.raises(ValueError):
+        ww.wl_gemv_batched(L, case.packed_d, case.scales_d, Z[:, ::2])
+    with pytest.raises(ValueError):
+        ww.wl_gemv(L, case.packed_d[:-16], case.scales_d, case.x_d[0], y)
+    with pytest.raises(ValueError):
+        ww.wl_gemv(L, case.packed_d, case.scales_d[:4], case.x_d[0], y)
     X = torch.zeros((17, 32), dtype=torch.complex64, device="cuda")
     with pytest.raises(ww.WWError) as e:
         ww.wl_gemv_batched(L, case.packed_d, case.scales_d, X)
@@ -303,3 +315,56 @@ def test_many_rows_per_cta(n):
     assert li["path"] == (0 if n == 200_000 else 1)
     for conv in CONVS:
         assert_parity(case.gpu(ww, torch, conv), case.oracle(ORC[conv]), case)
+
+
+@pytest.mark.parametrize("B", [1, 6])
+@pytest.mark.parametrize("graph", [False, True])
+def test_pdl_chain_reads_previous_layers_output(B, graph):
+    # layer 2 reads layer 1's y as its x and layer 3 reads it as its per-row scales,
+    # all launched with WW_FLAG_PDL on one stream (the next kernel starts while the previous
+    # one runs).  y1 is poisoned with NaN before every run, so a read before
+    # griddepcontrol.wait would show up; results must equal the same chain without PDL, bitwise.
+    n2, m1 = 300, 1000
+    n1 = 2 * n2  # y1 as float32 = n2 x 4 scales
+    c1 = LayerCase(n1, m1, seed=31, B=B).device(ww, torch)
+    c2 = LayerCase(n2, n1, seed=32, B=B).device(ww, torch)
+    c3 = LayerCase(n2, m1, seed=33, B=B).device(ww, torch)
+    s = torch.cuda.Stream()
+
+    def chain(flags, Y1, Y2, Y3):
+        L1, L2, L3 = c1.layer(ww, 0, flags), c2.layer(ww, 0, flags), c3.layer(ww, 0, flags)
+        ww.wl_gemv_batched(L1, c1.packed_d, c1.scales_d, c1.x_d, Y1, stream=s)
+        ww.wl_gemv_batched(L2, c2.packed_d, c2.scales_d, Y1, Y2, stream=s)
+        sc3 = torch.view_as_real(Y1[0]).reshape(n2, 4)
+        ww.wl_gemv_batched(L3, c3.packed_d, sc3, c3.x_d, Y3, stream=s)
+
+    def bufs():
+        return [torch.full((B, n), float("nan"), dtype=torch.complex64, device="cuda")
+                for n in (n1, n2, n2)]
+
+    ref = bufs()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        chain(0, *ref)
+    torch.cuda.synchronize()
+    assert not any(torch.isnan(torch.view_as_real(r)).any() for r in ref)
+    got = bufs()
+    torch.cuda.synchronize()
+    if graph:
+        with torch.cuda.stream(s):
+            chain(ww.FLAG_PDL, *got)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            chain(ww.FLAG_PDL, *got)
+    for _ in range(5):
+        with torch.cuda.stream(s):
+            for t in got:
+                t.fill_(float("nan"))
+            if graph:
+                g.replay()
+            else:
+                chain(ww.FLAG_PDL, *got)
+        torch.cuda.synchronize()
+        for a, b in zip(ref, got):
+            assert torch.equal(torch.view_as_real(a), torch.view_as_real(b))

@@ -368,3 +368,56 @@ def test_op_counts_lane_split():
                        np.ones(m, np.complex64))
     assert c["adds"] == 32 and c["subs"] == 0  # U_re mask drives the re and im path (O1)
     assert c["slots"] == 8 * n * m and c["scale_muls"] == 8
+
+
+# ---------------------------------------------------------------- two-phase dense form
+
+def _dense(planar, n, m, scales, x, conv, omp, rows=None):
+    U, Wd = orc.build_dense(planar, n, m, scales, rows, omp=omp)
+    return orc.eval_dense(U, Wd, x, conv, omp=omp)
+
+
+@pytest.mark.parametrize("omp", [False, True])
+@pytest.mark.parametrize("ex", _golden(), ids=lambda e: e["name"])
+def test_dense_form_worked_examples(ex, omp):
+    # the phase-split form (CPU-baseline timing) reproduces the hand-worked values exactly
+    n, m = ex["n"], ex["m"]
+    planar = orc.pack_planar(np.stack([np.array(ex[p], np.int8) for p in PLANES]))
+    scales = (np.array(ex["scales_per_row"], np.float32) if "scales_per_row" in ex
+              else np.array(ex["scales_per_tensor"], np.float32))
+    x = np.array([complex(a, b) for a, b in ex["x"]], np.complex64)
+    for conv, key in ((orc.CONV_EQ1, "y_EQ1"), (orc.CONV_ALG1, "y_ALG1")):
+        want = np.array([complex(a, b) for a, b in ex[key]])
+        assert np.array_equal(_dense(planar, n, m, scales, x, conv, omp)[0], want)
+
+
+@pytest.mark.parametrize("omp", [False, True])
+def test_dense_form_w_zero_is_zgemv(omp):
+    n, m = 41, 90
+    planes, _, scales, x = _rand_layer(12, n, m)
+    planes[2:] = 0
+    U = scales[:, 0:1].astype(np.float64) * planes[0] + 1j * scales[:, 1:2] * planes[1]
+    got = _dense(orc.pack_planar(planes), n, m, scales, x, orc.CONV_EQ1, omp)[0]
+    np.testing.assert_allclose(got, U @ x.astype(np.complex128), rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("conv", [orc.CONV_EQ1, orc.CONV_ALG1])
+def test_dense_form_bitwise_equals_direct_any_thread_count(conv):
+    n, m = 203, 517
+    planes, planar, scales, _ = _rand_layer(13, n, m)
+    x = wi.activations(13, m, 3)
+    want = orc.wl_direct(planar, n, m, scales, x, conv)
+    for omp in (False, True):
+        assert np.array_equal(_dense(planar, n, m, scales, x, conv, omp), want)
+    rows = np.array([202, 0, 17, 17, 100])
+    assert np.array_equal(_dense(planar, n, m, scales, x, conv, True, rows),
+                          orc.wl_direct(planar, n, m, scales, x, conv, rows))
+    assert orc.num_threads(False) == 1 and orc.num_threads(True) >= 1
+
+
+def test_dense_form_rejects_invalid_encoding():
+    n, m = 3, 16
+    planar = orc.pack_planar(np.zeros((4, n, m), np.int8))
+    planar[1, 2, 0] = 0x3  # slot 0 of row 2 = (1,1)
+    with pytest.raises(orc.OracleError):
+        orc.build_dense(planar, n, m, np.ones((n, 4), np.float32), omp=True)

@@ -35,9 +35,15 @@ def _stale(out, srcs):
 def build_oracle(force=False):
     src = os.path.join(ROOT, "oracle", "oracle.c")
     out = os.path.join(ROOT, "oracle", "liboracle.so")
-    if force or _stale(out, [src, os.path.join(ROOT, "oracle", "oracle.h")]):
+    deps = [src, os.path.join(ROOT, "oracle", "oracle.h")]
+    if force or _stale(out, deps):
         _run(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-Wall",
-              "-o", out, src, "-lm"])
+              "-Wno-unknown-pragmas", "-o", out, src, "-lm"])
+    # the same source with OpenMP over rows (CPU baseline's all-core mode; same results)
+    out_omp = os.path.join(ROOT, "oracle", "liboracle_omp.so")
+    if force or _stale(out_omp, deps):
+        _run(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-Wall",
+              "-fopenmp", "-o", out_omp, src, "-lm"])
 
 
 def build_inputs(force=False):
