@@ -241,13 +241,28 @@ def run_ours(args, world, rank, local):
     group = dist.group.WORLD if world > 1 else None
 
     if args.workload == "c4":
-        stack = WLStack(layers=args.layers, seed=args.seed, B=args.batch, rank=rank, world=world,
-                        pdl=not args.no_pdl, device=dev, group=group, fuse=not args.no_fuse)
+        base = WLStack(layers=args.layers, seed=args.seed, B=args.batch, rank=rank, world=world,
+                       pdl=not args.no_pdl, device=dev, group=group, fuse=not args.no_fuse)
+        if args.engine == "program":
+            stack = ProgramRunner(base, args.chain, args.seed)
+        else:
+            if args.chain != "plain":
+                raise SystemExit("--chain block needs --engine program")
+            stack = base
         units = [stack]
         layers_per_step = 7 * args.layers  # widely-linear projections per token
-        workload = (f"c4_llama2_7b_wl_decode_stack ({args.layers} layers x 7 projections, "
-                    + ("q/k/v and gate/up launched together per shared input: 4 launches per "
-                       "layer" if not args.no_fuse else "one launch per projection") + ")")
+        if args.engine == "program":
+            workload = (f"c4_llama2_7b_wl_decode_stack ({args.layers} layers x 7 projections, "
+                        "one persistent program launch per token: 4 stages per layer, "
+                        + ("each stage's own seeded x, stage i+1 waits for stage i"
+                           if args.chain == "plain" else
+                           "NEXT-3 decode blocks chained (RMSNorm, identity attention, "
+                           "residuals, SiLU(gate)*up fused)") + ")")
+        else:
+            workload = (f"c4_llama2_7b_wl_decode_stack ({args.layers} layers x 7 projections, "
+                        + ("q/k/v and gate/up launched together per shared input: 4 launches "
+                           "per layer" if not args.no_fuse else "one launch per projection")
+                        + ")")
     else:
         # single-layer configs: R replicas of the layer (>= 4x L2) cycled inside a step
         spec = {"c2": wi.C2, "c3a": wi.C3A, "c3b": wi.C3B, "c5": wi.C3B, "c1": wi.C1}[args.workload]
@@ -326,7 +341,7 @@ def run_ours(args, world, rank, local):
     per_shape = {}
     allgather_us = {}
     kern_ms_total = 0.0
-    if args.workload == "c4":
+    if args.workload == "c4" and args.engine == "pdl":
         kinds = {}
         for i, st in enumerate(stack.stages):
             kinds.setdefault(st.name, []).append(i)
@@ -381,7 +396,8 @@ def run_ours(args, world, rank, local):
     roof = {"bound": "alu", "achieved": round(achieved_alu, 4), "peak": round(alu_peak, 4),
             "unit": "Tadd/s", "frac": round(achieved_alu / alu_peak, 4),
             "traffic": _ncu_traffic(),
-            "kernel": "wl_gemv_kernel<1>",
+            "kernel": ("wl_program_kernel (whole step)" if args.engine == "program"
+                       and args.workload == "c4" else "wl_gemv_kernel<1>"),
             "peak_basis": f"128 fp32 add lanes/clk/SM x {nsm} SMs x {sm_mhz:.0f} MHz (DESIGN.md §8)",
             "hbm": {"achieved": round(hbm_achieved, 1), "peak": peaks.get("hbm_gbs"),
                     "unit": "GB/s", "frac": round(hbm_achieved / peaks.get("hbm_gbs", 6650.0), 4),
@@ -470,7 +486,7 @@ def _e2e(stack, args, s, dev, graph, world, alg_bytes):
     -> HBM each step, the last projection's gathered output -> host each step."""
     import torch
     import torch.distributed as dist
-    xflat = stack.X.view(-1)
+    xflat = (stack.inputs() if hasattr(stack, "inputs") else stack.X).view(-1)
     xh = torch.empty(xflat.numel(), dtype=torch.complex64).pin_memory()
     xh.copy_(xflat.cpu())
     last = stack.Y[-1]
@@ -511,6 +527,43 @@ def _launch_configs(ww, stack, args):
     else:
         shapes = {f"{stack.spec.name} {stack.nloc}x{stack.spec.m}": (stack.nloc, stack.spec.m)}
     return {k: ww.query_launch(ww.Layer(max(n, 1), m), args.batch) for k, (n, m) in shapes.items()}
+
+
+class ProgramRunner:
+    """The C4 stack as ONE persistent program launch per token (ww_program_run): the same
+    weights, scales and gathered outputs as the per-launch WLStack."""
+
+    def __init__(self, base, chain, seed):
+        import torch
+        import paper_2604_20913_b200 as ww
+        from paper_2604_20913_b200.stack import block_gammas, program_stages
+        if base.world != 1:
+            raise SystemExit("--engine program at world > 1 needs peer-mapped outputs (not wired "
+                             "in bench.py); use the default engine")
+        self.base, self.chain = base, chain
+        gam = None
+        if chain == "block":
+            gam = [tuple(torch.from_numpy(g).to(base.device) for g in pair)
+                   for pair in block_gammas(seed, base.layers, 2048)]
+        self.gam = gam
+        self.prog = ww.Program([program_stages(base, [base], chain, gam)], world=1)
+        self.stages, self.X, self.Y = base.stages, base.X, base.Y
+
+    def step(self, stream=None):
+        self.prog.run(stream)
+        return 1
+
+    def inputs(self):
+        return self.base.X if self.chain == "plain" else self.base.X[:self.base.stages[0].m]
+
+    def algorithmic_bytes(self):
+        return self.base.algorithmic_bytes()
+
+    def packed_act_bytes(self):
+        return self.base.packed_act_bytes()
+
+    def adds(self):
+        return self.base.adds()
 
 
 class _ReplicaLayer:
@@ -605,6 +658,10 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--no-fuse", action="store_true",
                     help="c4: one launch per projection instead of one per shared input")
+    ap.add_argument("--engine", choices=("pdl", "program"), default="pdl",
+                    help="c4: PDL-chained launches per stage, or one persistent program launch")
+    ap.add_argument("--chain", choices=("plain", "block"), default="plain",
+                    help="c4 program: independent seeded stage inputs, or NEXT-3 decode blocks")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")

@@ -170,6 +170,81 @@ ww_status ww_ternary_gemv_plane(int64_t n, int64_t m, const void* planar_d, int3
 ww_status ww_wl_combine(const ww_layer* L, const float* acc8_d, const float* scales_d, float* y_d,
                         void* stream);
 
+/* ------------------------------------------------------------------------------------
+ * Persistent stage-chained program (DESIGN.md §6 "program kernel"): one cooperative launch
+ * runs `nstages` widely-linear layers (B = 1) in order, e.g. one decode step of the
+ * config-4 stack.  Stage s may read what stage s-1 wrote (wait = 1): the dependency is a
+ * readiness counter per rank instead of a kernel boundary (the fork/join removal of P:1022-
+ * 1026 applied across layers), while every CTA's producer warp keeps streaming the next
+ * stages' packed weights into shared memory.  Output rows are stored straight into the
+ * gathered output of every rank (`y[g]`, peer-mapped device pointers at world > 1): the
+ * all-gather of the row-sharded layer is fused into the GEMV
+ * epilogue.  Fused ops for the decode block:
+ *   prologue WW_PRO_RMSNORM: x <- x * gamma / sqrt(mean(x^2) + eps) over the real 2m-vector
+ *     (re, im interleaved, gamma = 2m fp32), WW_PRO_MUL: x <- x (.) x2 (re*re, im*im);
+ *   epilogue WW_EPI_RESIDUAL: y_i += residual_i, WW_EPI_SILU: rows i < silu_rows get
+ *     (silu(re), silu(im)), silu(v) = v / (1 + exp(-v)).
+ * Requirements: 16 | m, x / x2 / packed / scales 16-B aligned, y / residual 8-B aligned,
+ * world <= WW_PROG_MAX_RANKS, the stage's x of at most WW_PROG_MAX_M columns.  Outputs of
+ * a stage are its gathered rows [row0, row0 + n_local) in every y[g] (g < world).
+ * `ranks_in_launch` > 1 runs several ranks' shards in ONE launch on one GPU (CTAs split
+ * evenly between them; used to test the multi-rank protocol without several GPUs).
+ * ------------------------------------------------------------------------------------ */
+#define WW_PROG_MAX_RANKS 8
+#define WW_PROG_MAX_M 11264 /* 22 x 512 columns: x (and x2) of a stage in shared memory */
+#define WW_PRO_NONE 0
+#define WW_PRO_RMSNORM 1
+#define WW_PRO_MUL 2
+#define WW_EPI_NONE 0
+#define WW_EPI_RESIDUAL 1
+#define WW_EPI_SILU 2
+
+typedef struct {
+    const void* packed;   /* this rank's WW_LAYOUT_COL4 rows [row0, row0 + n_local) */
+    const float* scales;  /* their scales: n_local x 4 (per row) or 4 (per tensor) */
+    int64_t n_local;      /* rows this rank computes (>= 0) */
+    int64_t row0;         /* global index of its first row */
+    int64_t m;            /* complex input columns */
+    int32_t scale_mode;   /* ww_scale_mode */
+    int32_t conv;         /* ww_convention */
+    const float* x;       /* complex64[m] input on this rank */
+    const float* x2;      /* WW_PRO_MUL: second complex64[m] operand, else NULL */
+    float* y[WW_PROG_MAX_RANKS]; /* complex64 gathered output on rank g (g < world) */
+    const float* residual;       /* WW_EPI_RESIDUAL: complex64 indexed by global row */
+    const float* gamma;          /* WW_PRO_RMSNORM: 2m fp32 */
+    float eps;                   /* WW_PRO_RMSNORM */
+    int32_t prologue;            /* WW_PRO_* */
+    int32_t epilogue;            /* WW_EPI_* */
+    int32_t wait;                /* 1: x depends on earlier stages of the program */
+    int64_t silu_rows;           /* WW_EPI_SILU: global rows below this get SiLU */
+} ww_stage;
+
+/* Host-side handle filled by ww_program_init (caller-owned POD; keep it with the
+ * workspace).  Launch geometry: grid = ranks_in_launch x ctas_per_rank CTAs of `block`
+ * threads (16 consumer warps + 1 producer warp), `smem_bytes` of shared memory, a weight
+ * ring of `nslot` slots of `slot_bytes`. */
+typedef struct {
+    int32_t nstages, world, rank_base, ranks_in_launch;
+    int32_t grid, block, smem_bytes, ctas_per_rank, nslot, slot_bytes, x_bytes, has_mul;
+    void* workspace;                         /* device descriptors (caller-allocated) */
+    uint32_t* sync[WW_PROG_MAX_RANKS];       /* device sync words of every rank */
+} ww_program;
+
+/* Device workspace bytes for nstages x ranks_in_launch stage descriptors (128-B aligned). */
+size_t ww_program_workspace_bytes(int32_t nstages, int32_t ranks_in_launch);
+/* Bytes of one rank's sync words; caller-allocated, 128-B aligned, ZERO-initialised once
+ * (at world > 1 in memory every rank can reach: sync_d[g] is rank g's block as seen here). */
+size_t ww_program_sync_bytes(void);
+/* Validate the stages (stages[r * nstages + s] = stage s of rank rank_base + r), encode the
+ * TMA maps and copy the descriptors into workspace_d (synchronous).  Errors before any
+ * device work: WW_ERR_INVALID_ARGUMENT / WW_ERR_MISALIGNED / WW_ERR_UNSUPPORTED. */
+ww_status ww_program_init(const ww_stage* stages, int32_t nstages, int32_t world,
+                          int32_t rank_base, int32_t ranks_in_launch, uint32_t* const* sync_d,
+                          void* workspace_d, ww_program* out);
+/* Launch the program (asynchronous on `stream`; cooperative launch, all CTAs co-resident).
+ * Every rank must launch the same program the same number of times. */
+ww_status ww_program_run(const ww_program* prog, void* stream);
+
 const char* ww_status_string(ww_status s);
 const char* ww_last_error(void); /* thread-local message of the last failing call */
 int32_t ww_version(void);

@@ -225,3 +225,72 @@ def tolerance_check(y, y_ref, scales, x, n_rows_idx=None):
     ratio = np.maximum(np.abs(err.real), np.abs(err.imag)) / np.maximum(bound, 1e-300)
     worst = float(ratio.max()) if ratio.size else 0.0
     return (rel <= 1e-5 and worst <= 1.0), float(rel), worst
+
+
+# --------------------------------------------------------------------------- decode block (NEXT-3)
+# Plain numpy fp64, following SPEC's pipeline module ("artifact plumbing" ops the
+# paper's App. J lists).  Readings (R11): activations are the real
+# 2m-vector viewed as m complex numbers (re, im interleaved, as complex64 memory is), so the
+# non-GEMV ops act on that real vector: RMSNorm over all 2m reals with a 2m-entry gamma,
+# SiLU and the (.) product on re and im separately; attention is the identity on v.
+
+def _real(z):
+    z = np.asarray(z)
+    return np.stack([z.real, z.imag], axis=-1).reshape(*z.shape[:-1], -1).astype(np.float64)
+
+
+def _cplx(v):
+    v = np.asarray(v, dtype=np.float64)
+    return v[..., 0::2] + 1j * v[..., 1::2]
+
+
+def rmsnorm(x, gamma, eps=1e-5):
+    """y_i = x_i * gamma_i / sqrt(mean(x^2) + eps) over the real 2m-vector."""
+    v = _real(x)
+    r = 1.0 / np.sqrt(np.mean(v * v, axis=-1, keepdims=True) + eps)
+    return _cplx(v * np.asarray(gamma, np.float64) * r)
+
+
+def silu(v):
+    """S:491-498: x * sigmoid(x) = x / (1 + exp(-x))."""
+    v = np.asarray(v, dtype=np.float64)
+    return v / (1.0 + np.exp(-v))
+
+
+def silu_c(z):
+    """SiLU of a complex vector's real view: (silu(re), silu(im))."""
+    z = np.asarray(z)
+    return silu(z.real) + 1j * silu(z.imag)
+
+
+def mul_c(a, b):
+    """The (.) of SiLU(gate) (.) up on the real view: (a_re b_re, a_im b_im)."""
+    a, b = np.asarray(a), np.asarray(b)
+    return a.real.astype(np.float64) * b.real + 1j * (a.imag.astype(np.float64) * b.imag)
+
+
+def wl_dense_apply(U, Wd, x, conv=CONV_EQ1):
+    """The widely-linear map on dense fp64 rows (orc_build_dense) for an fp64 complex x:
+    Eq. 1 (EQ1) or (U + conj W) x (ALG1, Eqs. 2-3) -- numpy complex128 matmul."""
+    x = np.asarray(x, dtype=np.complex128)
+    if conv == CONV_EQ1:
+        return U @ x + Wd @ np.conj(x)
+    return (U + np.conj(Wd)) @ x
+
+
+def block_forward(layer, h, gammas, eps=1e-5, conv=CONV_EQ1):
+    """One decode block: rmsnorm -> qkv -> identity attention (v) -> o ->
+    residual -> rmsnorm -> gate/up -> silu(gate) (.) up -> down -> residual.
+    layer: dict proj -> (U, Wd) dense rows from build_dense (q, k, v, o, gate, up, down);
+    h: complex (m,).  Returns (h_out, intermediates dict)."""
+    xa = rmsnorm(h, gammas[0], eps)
+    q = wl_dense_apply(*layer["q"], xa, conv)
+    k = wl_dense_apply(*layer["k"], xa, conv)
+    v = wl_dense_apply(*layer["v"], xa, conv)
+    h1 = wl_dense_apply(*layer["o"], v, conv) + h
+    xm = rmsnorm(h1, gammas[1], eps)
+    gate = wl_dense_apply(*layer["gate"], xm, conv)
+    up = wl_dense_apply(*layer["up"], xm, conv)
+    a = mul_c(silu_c(gate), up)
+    h2 = wl_dense_apply(*layer["down"], a, conv) + h1
+    return h2, {"q": q, "k": k, "v": v, "h1": h1, "gate": gate, "up": up, "act": a, "h2": h2}

@@ -33,11 +33,17 @@ SCALES_PER_TENSOR, SCALES_PER_ROW = 0, 1
 FLAG_PDL = 1
 MAX_BATCH = 16
 
+PROG_MAX_RANKS = 8
+PROG_MAX_M = 11264
+PRO_NONE, PRO_RMSNORM, PRO_MUL = 0, 1, 2
+EPI_NONE, EPI_RESIDUAL, EPI_SILU = 0, 1, 2
+
 # every symbol include/ww.h declares (tests check the library exports them all)
 EXPORTS = ("ww_packed_bytes", "ww_pack_ternary", "ww_unpack_ternary", "ww_repack",
            "ww_pack_ternary_device", "ww_wl_gemv", "ww_wl_gemv_batched", "ww_shard_plan",
            "ww_query_launch", "ww_status_string", "ww_last_error", "ww_version",
-           "ww_ternary_gemv_plane", "ww_wl_combine")
+           "ww_ternary_gemv_plane", "ww_wl_combine", "ww_program_workspace_bytes",
+           "ww_program_sync_bytes", "ww_program_init", "ww_program_run")
 
 
 class WWError(RuntimeError):
@@ -64,6 +70,25 @@ class _LaunchInfo(ctypes.Structure):
                                               "tile_chunks", "num_sms", "parts", "split_chunks", "path")]
 
 
+class _Stage(ctypes.Structure):
+    _fields_ = [("packed", ctypes.c_void_p), ("scales", ctypes.c_void_p),
+                ("n_local", ctypes.c_int64), ("row0", ctypes.c_int64), ("m", ctypes.c_int64),
+                ("scale_mode", ctypes.c_int32), ("conv", ctypes.c_int32),
+                ("x", ctypes.c_void_p), ("x2", ctypes.c_void_p),
+                ("y", ctypes.c_void_p * PROG_MAX_RANKS),
+                ("residual", ctypes.c_void_p), ("gamma", ctypes.c_void_p),
+                ("eps", ctypes.c_float), ("prologue", ctypes.c_int32),
+                ("epilogue", ctypes.c_int32), ("wait", ctypes.c_int32),
+                ("silu_rows", ctypes.c_int64)]
+
+
+class _Program(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in (
+        "nstages", "world", "rank_base", "ranks_in_launch", "grid", "block", "smem_bytes",
+        "ctas_per_rank", "nslot", "slot_bytes", "x_bytes", "has_mul")] + [
+        ("workspace", ctypes.c_void_p), ("sync", ctypes.c_void_p * PROG_MAX_RANKS)]
+
+
 _i64, _i32, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
 _lib.ww_packed_bytes.restype = ctypes.c_size_t
 _lib.ww_packed_bytes.argtypes = [_i64, _i64]
@@ -88,6 +113,15 @@ _lib.ww_ternary_gemv_plane.restype = _i32
 _lib.ww_ternary_gemv_plane.argtypes = [_i64, _i64, _vp, _i32, _vp, _i32, _vp, ctypes.c_uint32, _vp]
 _lib.ww_wl_combine.restype = _i32
 _lib.ww_wl_combine.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _vp]
+_lib.ww_program_workspace_bytes.restype = ctypes.c_size_t
+_lib.ww_program_workspace_bytes.argtypes = [_i32, _i32]
+_lib.ww_program_sync_bytes.restype = ctypes.c_size_t
+_lib.ww_program_sync_bytes.argtypes = []
+_lib.ww_program_init.restype = _i32
+_lib.ww_program_init.argtypes = [ctypes.POINTER(_Stage), _i32, _i32, _i32, _i32,
+                                 ctypes.POINTER(_vp), _vp, ctypes.POINTER(_Program)]
+_lib.ww_program_run.restype = _i32
+_lib.ww_program_run.argtypes = [ctypes.POINTER(_Program), _vp]
 _lib.ww_status_string.restype = ctypes.c_char_p
 _lib.ww_status_string.argtypes = [_i32]
 _lib.ww_last_error.restype = ctypes.c_char_p
@@ -291,3 +325,82 @@ def wl_gemv_unfused(layer: Layer, planar, scales, x, y=None, acc=None, stream=No
     L = layer.c()
     _check(_lib.ww_wl_combine(ctypes.byref(L), acc.data_ptr(), scales.data_ptr(), y.data_ptr(), s))
     return y
+
+
+# --------------------------------------------------------------------------- program
+@dataclass
+class Stage:
+    """One stage of a persistent program (ww_stage); tensors are CUDA tensors.
+    y: list of the gathered complex64 output buffers of every rank (index = rank)."""
+    packed: object
+    scales: object
+    n_local: int
+    row0: int
+    m: int
+    x: object
+    y: list
+    scale_mode: int = SCALES_PER_ROW
+    conv: int = CONV_EQ1
+    x2: object = None
+    residual: object = None
+    gamma: object = None
+    eps: float = 1e-5
+    prologue: int = PRO_NONE
+    epilogue: int = EPI_NONE
+    wait: int = 1
+    silu_rows: int = 0
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+class Program:
+    """ww_program_init / ww_program_run: `stages[r][s]` = stage s of rank rank_base + r.
+    ranks_in_launch = len(stages) ranks run in one launch (one GPU); `sync` is a list of
+    `world` device tensors of ww_program_sync_bytes() zeroed bytes (rank g's sync words)."""
+
+    def __init__(self, stages, world: int = 1, rank_base: int = 0, sync=None, device=None):
+        import torch
+        R, S = len(stages), len(stages[0])
+        assert all(len(st) == S for st in stages)
+        dev = device if device is not None else stages[0][0].x.device
+        self.world, self.R, self.S = world, R, S
+        nbytes = int(_lib.ww_program_workspace_bytes(S, R))
+        self.workspace = torch.empty(nbytes + 128, dtype=torch.uint8, device=dev)
+        ws = self.workspace.data_ptr()
+        ws_al = (ws + 127) // 128 * 128
+        sb = int(_lib.ww_program_sync_bytes())
+        if sync is None:
+            self._sync_buf = torch.zeros(world * sb + 128, dtype=torch.uint8, device=dev)
+            b = (self._sync_buf.data_ptr() + 127) // 128 * 128
+            sync_ptrs = [b + g * sb for g in range(world)]
+        else:
+            self._sync_buf = sync
+            sync_ptrs = [t if isinstance(t, int) else t.data_ptr() for t in sync]
+        self._keep = []
+        arr = (_Stage * (R * S))()
+        for r in range(R):
+            for s_, st in enumerate(stages[r]):
+                c = arr[r * S + s_]
+                c.packed, c.scales = _ptr(st.packed), _ptr(st.scales)
+                c.n_local, c.row0, c.m = st.n_local, st.row0, st.m
+                c.scale_mode, c.conv = st.scale_mode, st.conv
+                c.x, c.x2 = _ptr(st.x), _ptr(st.x2)
+                for g in range(world):
+                    yg = st.y[g]
+                    c.y[g] = yg if isinstance(yg, int) else yg.data_ptr()
+                c.residual, c.gamma, c.eps = _ptr(st.residual), _ptr(st.gamma), st.eps
+                c.prologue, c.epilogue, c.wait, c.silu_rows = (st.prologue, st.epilogue, st.wait,
+                                                               st.silu_rows)
+                self._keep.append(st)
+        sp = (_vp * world)(*sync_ptrs)
+        self.prog = _Program()
+        _check(_lib.ww_program_init(arr, S, world, rank_base, R, sp, ws_al, ctypes.byref(self.prog)))
+        torch.cuda.synchronize(dev)
+
+    def info(self) -> dict:
+        return {f: getattr(self.prog, f) for f, _ in _Program._fields_[:12]}
+
+    def run(self, stream=None):
+        _check(_lib.ww_program_run(ctypes.byref(self.prog), _stream_ptr(stream)))

@@ -3,7 +3,9 @@
 // function) pair, so they are cached per device behind a mutex: a process that drives
 // several GPUs from one or many threads gets each device's own values (ww.h: thread-safe,
 // no global state besides caches keyed by device and the thread-local error string).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <mutex>
 #include <set>
@@ -57,6 +59,39 @@ int prepare_kernel(const void* fn, int max_dynamic_smem) {
     if (e != cudaSuccess) return (int)e;
     g_prepared.insert({dev, fn});
     return 0;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link); the
+// entry point is process-wide (not per device): resolved once, thread-safe
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        return nullptr;
+    }();
+    return fn;
+}
+
+// x viewed as a [B][W][32 floats] tensor (one 128-byte row per 16-column chunk); boxes of
+// 32 chunks x 128 B land 128B-swizzled, i.e. granule g of chunk tc at g ^ (tc & 7) -- the
+// layout the sweep reads.  Chunks past W (the last box's tail) are zero-filled.  Needs a
+// 16-B aligned x and 16 | m (checked by the callers).
+int encode_x_map(void* map, const float* X, int64_t W, int64_t B, int64_t ldx) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return -1;
+    const cuuint64_t dims[3] = {32, (cuuint64_t)W, (cuuint64_t)B};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)ldx * 8};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                     const_cast<float*>(X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
 }  // namespace ww

@@ -13,4 +13,6 @@ ww_status ok();
 int current_device();
 int device_sms();                                          // SM count of the current device
 int prepare_kernel(const void* fn, int max_dynamic_smem);  // cudaError_t of the attribute calls
+// CUtensorMap of x as [B][W][32 floats], 32 x 32 boxes, 128B swizzle (0 on success)
+int encode_x_map(void* map, const float* X, int64_t W, int64_t B, int64_t ldx);
 }  // namespace ww

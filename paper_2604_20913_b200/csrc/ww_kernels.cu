@@ -27,6 +27,7 @@
 
 #include "ww.h"
 #include "ww_internal.h"
+#include "ww_sweep.cuh"
 
 #ifndef WW_DEBUG_FLAGS
 #define WW_DEBUG_FLAGS 0  // 1: honour Params::dbg (tools/chain_time.py builds build/libww_dbg.so)
@@ -44,67 +45,11 @@ constexpr int kGroup = 4;                  // batches above this run as groups o
 constexpr int64_t kSmemBudget = 226 * 1024; // single-tile path: all shared memory of a CTA
 constexpr int kPrefetch = 2;                 // L2 prefetch distance beyond the weight loads
 
-// ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
-}
-
-// the same load, issued only when a < b (else zeros): one compare + one predicated LDG
-__device__ __forceinline__ uint4 ldg_stream_lt(const uint4* p, int a, int b) {
-    uint4 v = make_uint4(0, 0, 0, 0);
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %5, %6;\n\t"
-        "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
-        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-        : "l"(p), "r"(a), "r"(b));
-    return v;
-}
-
-__device__ __forceinline__ float4 lds128(uint32_t addr) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(addr));
-    return v;
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
-
-// L2 prefetch of the 16-byte chunk at p when a < b (one compare + one predicated PREFETCH)
-__device__ __forceinline__ void prefetch_chunk_lt(const uint4* p, int a, int b) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %1, %2;\n\t@q prefetch.global.L2 [%0];\n\t}"
-        :: "l"(p), "r"(a), "r"(b));
-}
-
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() {
-    asm volatile("griddepcontrol.launch_dependents;" :::);
-}
 #if WW_DEBUG_FLAGS
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 #endif
-
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
 #ifdef WW_TRACE
 // per-warp event timestamps (globaltimer ns) for tools/trace_kernel.py; not in the product build
@@ -147,51 +92,6 @@ struct alignas(64) Params {
                           // 2 = skip the accumulation, 8 = bulk L2 prefetch of the CTA's
                           // weights at kernel start (overhead measurement); 0 in the product
 };
-
-__host__ __device__ constexpr int next_pow2(int v) {
-    int p = 1;
-    while (p < v) p <<= 1;
-    return p;
-}
-
-// TMA (cp.async.bulk.tensor) load of one 32-chunk x box into shared memory, completing
-// `bytes` of transaction on mbarrier `bar`
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                            int c2, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void fence_barrier_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-// mbarrier helpers (one barrier per 32-chunk x slice; completes once per launch, phase 0)
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void mbar_wait0(uint32_t bar) { mbar_wait(bar, 0); }
-
 
 // cp.async of one 16-byte x granule (columns col, col+1 of vector row `src`), zero-filling
 // columns >= m (R6)
@@ -260,139 +160,6 @@ __device__ __forceinline__ void stage_x_regions_tma(const Params& p, uint32_t xs
         for (int b = 0; b < B; ++b)
             tma_load_3d(xs + (uint32_t)((b * J + j) * 4096), &p.tmap, 0, 32 * j, b, bar);
     }
-}
-
-// Accumulators: S column-parity sets of B x 4 pair sums.  For B <= 2 even and odd columns
-// feed separate sets (more independent FADD2 chains per warp, half-length fp32 chains);
-// larger B has ILP across vectors.  (Separate sums of the +1 and the -1 codes measured
-// 5-10 % slower: register pressure.)
-template <int B>
-struct Acc {
-    static constexpr int S = B <= 2 ? 2 : 1;  // column-parity sets
-    static constexpr int N = 1;
-    float2 a[S][N][B][4];
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int k = 0; k < N; ++k)
-#pragma unroll
-                for (int b = 0; b < B; ++b)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) a[s][k][b][q] = make_float2(0.f, 0.f);
-    }
-    // sum over sets of plane q, vector b (pos - neg when N == 2)
-    __device__ __forceinline__ float2 total(int b, int q) const {
-        float2 t = a[0][0][b][q];
-        if (S == 2) t = fadd2(t, a[S - 1][0][b][q]);
-        if (N == 2) {
-            float2 n = a[0][N - 1][b][q];
-            if (S == 2) n = fadd2(n, a[S - 1][N - 1][b][q]);
-            t = fadd2(t, make_float2(-n.x, -n.y));
-        }
-        return t;
-    }
-};
-
-// One column (8 code bits = 4 planes) against one activation pair: Eq. 6 (bit 2p+1, add)
-// and Eq. 7 (bit 2p, subtract) for each plane p.
-template <int N>
-__device__ __forceinline__ void column(float2 (&pos)[4], float2 (&neg)[4], uint32_t bits, float2 x) {
-    const float2 nx = make_float2(-x.x, -x.y);
-    // bits in ascending order (bit 2q = -1 of plane q, bit 2q+1 = +1) so the compiler can
-    // turn a column's 8 predicates into one R2P of bits 0..6 plus one bit test
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int q = k >> 1;
-        if (bits & (1u << k)) {
-            if (k & 1) pos[q] = fadd2(pos[q], x);
-            else if (N == 2) neg[q] = fadd2(neg[q], x);
-            else pos[q] = fadd2(pos[q], nx);
-        }
-    }
-}
-
-// One 16-column chunk of one row (its 16-byte COL4 word w) against the staged x of that
-// chunk: 64 codes x B vectors, 2 predicated FADD2 per code and vector.  xl = smem address of
-// the chunk's x for vector 0 with the swizzle key in bits 4..6 (chunk base | (chunk & 7) << 4;
-// vector b at + b*bstride): granule kk (columns 2kk, 2kk+1) sits at xl ^ (kk << 4), one LOP3
-// per load (the 128B swizzle of the TMA boxes; 32 lanes on 32 chunks hit 32 banks).
-template <int B>
-__device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xl, uint32_t bstride) {
-    constexpr int S = Acc<B>::S, N = Acc<B>::N;
-    const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {  // column pair (2kk, 2kk+1)
-        const uint32_t word = w4[kk >> 1];
-        const uint32_t sh = (kk & 1) * 16;
-        const uint32_t bits_a = (word >> sh) & 0xffu, bits_b = (word >> (sh + 8)) & 0xffu;
-        const uint32_t xa = xl ^ ((uint32_t)kk << 4);
-#pragma unroll
-        for (int b = 0; b < B; ++b) {  // each decoded code drives all B vectors (a9)
-            const float4 v = lds128(xa + b * bstride);
-            // (odd column first: the same sums -- each column-parity set keeps its own
-            // order -- but ptxas then needs no predicate spill across the R2Ps)
-            column<N>(acc.a[S - 1][0][b], acc.a[S - 1][N - 1][b], bits_b, make_float2(v.z, v.w));
-            column<N>(acc.a[0][0][b], acc.a[0][N - 1][b], bits_a, make_float2(v.x, v.y));
-        }
-    }
-}
-
-// Transpose-reduce NV (power of 2) partial sums across the warp: after the halving rounds
-// lane l holds NV>>H totals starting at index (bit4(l) bit3(l) ...)_2 * (NV>>H).  Every
-// value is summed over the lanes in the same xor-butterfly order (16, 8, 4, 2, 1) for any
-// NV, so the totals do not depend on how many values are reduced together.
-template <int NV>
-__device__ __forceinline__ void warp_transpose_reduce(float (&v)[NV]) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-        const int off = 16 >> r;
-        const int cur = NV >> r;
-        if (cur > 1) {
-            const int half = cur / 2;
-            const bool up = (lane & off) != 0;
-#pragma unroll
-            for (int i = 0; i < half; ++i) {
-                const float send = up ? v[i] : v[i + half];
-                const float keep = up ? v[i + half] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-            }
-        } else {
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
-        }
-    }
-}
-
-// Warp reduction of this warp's 8B partial sums (a7): writes the NV = next_pow2(8B) totals
-// [A0.re A0.im A1.re A1.im A2.re A2.im A3.re A3.im] x B to smem `dst` (only the lanes that
-// hold them write).  Ends with __syncwarp.
-template <int B>
-__device__ __forceinline__ void reduce_to(const Acc<B>& acc, float* dst) {
-    const int lane = threadIdx.x & 31;
-    constexpr int NV = next_pow2(8 * B);
-    float v[NV];
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float2 t = acc.total(b, q);
-            v[8 * b + 2 * q] = t.x;
-            v[8 * b + 2 * q + 1] = t.y;
-        }
-#pragma unroll
-    for (int i = 8 * B; i < NV; ++i) v[i] = 0.f;
-    warp_transpose_reduce<NV>(v);
-    constexpr int H = NV >= 32 ? 5 : (NV >= 16 ? 4 : 3);
-    constexpr int C = NV >> H;
-    int idx = 0;
-#pragma unroll
-    for (int r = 0; r < H; ++r) idx = (idx << 1) | ((lane >> (4 - r)) & 1);
-    if ((lane & ((1 << (5 - H)) - 1)) == 0) {
-#pragma unroll
-        for (int s = 0; s < C; ++s) dst[idx * C + s] = v[s];
-    }
-    __syncwarp();
 }
 
 // Epilogue arithmetic (a8): the row's 8 scales applied once to its totals T of vector b
@@ -731,36 +498,9 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     return WW_OK;
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    // the driver entry point is process-wide (not per device); resolved once, thread-safe
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
-        void* ptr = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-        return nullptr;
-    }();
-    return fn;
-}
-
-// x viewed as a [B][W][32 floats] tensor (one 128-byte row per 16-column chunk); boxes of
-// 32 chunks x 128 B land 128B-swizzled, i.e. granule g of chunk tc at g ^ (tc & 7) -- the
-// layout chunk() reads.  Needs 16 | m, a 16-B aligned x and an even ldx (else cp.async).
 bool encode_x_map(Params& p, int B) {
     if (p.m % 16 != 0 || ((uintptr_t)p.X & 15) || (B > 1 && (p.ldx % 2) != 0)) return false;
-    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
-    if (!enc) return false;
-    const cuuint64_t dims[3] = {32, (cuuint64_t)p.W, (cuuint64_t)B};
-    const cuuint64_t strides[2] = {128, (cuuint64_t)p.ldx * 8};
-    const cuuint32_t box[3] = {32, 32, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p.X), dims,
-                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    return ww::encode_x_map(&p.tmap, p.X, p.W, B, p.ldx) == 0;
 }
 
 std::atomic<bool> g_force_rows{false};  // tests: run the row-by-row instantiation where kStream applies

@@ -205,3 +205,67 @@ class WLStack:
     def adds(self) -> int:
         """Algorithmic fp32 add/sub count on this rank (8 per complex column per row, App. D)."""
         return sum(8 * st.ylocal * st.m * self.B for st in self.stages)
+
+
+# ------------------------------------------------------------------ persistent program
+EPS = 1e-5
+
+
+def block_gammas(seed: int, layers: int, m: int):
+    """RMSNorm weights of the decode blocks (NEXT-3): per layer gamma_attn and gamma_mlp, each
+    2m fp32 (the real 2m-vector view), seeded ~ U[0.5, 1.5] (DESIGN.md input recipe)."""
+    out = []
+    for l in range(layers):
+        pair = []
+        for k in range(2):
+            s = wi.layer_seed(seed ^ 0x5EED, l, 100 + k)
+            pair.append(np.ascontiguousarray(wi.scales(s, m // 2, True, 0.5, 1.5).reshape(-1)))
+        out.append(tuple(pair))
+    return out
+
+
+def program_stages(part: "WLStack", parts: list, mode: str = "plain", gammas=None,
+                   x0=None):
+    """ww_stage list of one rank (`part`) for a persistent program over its WLStack; the
+    gathered outputs of rank g live in parts[g].Y.  mode "plain": every stage reads its own
+    seeded x (BASELINE config 4 as round 1 timed it) and waits for the previous stage;
+    mode "block": the NEXT-3 decode block chain -- per layer
+      qkv   x = RMSNorm(h_l; gamma_attn)            -> QKV_l
+      o     x = v = QKV_l[4096:6144], + residual h_l -> H1_l
+      gateup x = RMSNorm(H1_l; gamma_mlp), SiLU on the gate rows -> GU_l
+      down  x = SiLU(gate) (.) up = GU_l[:5504] (.) GU_l[5504:], + residual H1_l -> h_{l+1}
+    with h_0 = x0 (default: stage 0's seeded x).  gammas: block_gammas() as device tensors."""
+    from . import (EPI_NONE, EPI_RESIDUAL, EPI_SILU, PRO_MUL, PRO_NONE, PRO_RMSNORM,
+                   SCALES_PER_ROW, Stage)
+    world = part.world
+    assert part.B == 1 and len(parts) == world
+    st_list = []
+    for i, st in enumerate(part.stages):
+        ys = [parts[g].Y[i] for g in range(world)]
+        kw = dict(packed=part.W[st.off:st.off + max(st.nbytes, 16)],
+                  scales=part.S[st.soff:st.soff + max(4 * st.ylocal, 4)],
+                  n_local=st.ylocal, row0=st.shard.row_begin, m=st.m, y=ys,
+                  scale_mode=SCALES_PER_ROW, conv=part.conv, wait=1 if i > 0 else 0)
+        if mode == "plain":
+            kw.update(x=part.x_of(st)[0])
+        elif mode == "block":
+            Yl = part.Y  # this rank's copies of the gathered outputs
+            l = st.layer
+            base = 4 * l
+            h_l = (x0 if x0 is not None else part.x_of(part.stages[0])[0]) if l == 0 else Yl[base - 1]
+            if st.name == "qkv":
+                kw.update(x=h_l, prologue=PRO_RMSNORM, gamma=gammas[l][0], eps=EPS)
+            elif st.name == "o":
+                kw.update(x=Yl[base][4096:6144], epilogue=EPI_RESIDUAL, residual=h_l)
+            elif st.name == "gateup":
+                kw.update(x=Yl[base + 1], prologue=PRO_RMSNORM, gamma=gammas[l][1], eps=EPS,
+                          epilogue=EPI_SILU, silu_rows=5504)
+            elif st.name == "down":
+                kw.update(x=Yl[base + 2][:5504], x2=Yl[base + 2][5504:11008], prologue=PRO_MUL,
+                          epilogue=EPI_RESIDUAL, residual=Yl[base + 1])
+            else:
+                raise ValueError(st.name)
+        else:
+            raise ValueError(mode)
+        st_list.append(Stage(**kw))
+    return st_list

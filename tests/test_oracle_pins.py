@@ -421,3 +421,63 @@ def test_dense_form_rejects_invalid_encoding():
     planar[1, 2, 0] = 0x3  # slot 0 of row 2 = (1,1)
     with pytest.raises(orc.OracleError):
         orc.build_dense(planar, n, m, np.ones((n, 4), np.float32), omp=True)
+
+
+# ---------------------------------------------------------------- decode-block ops (NEXT-3)
+
+def test_rmsnorm_spec_examples():
+    # x = [3, 4] (RMS = sqrt(12.5)), gamma = 1, eps = 0 -> [0.8485, 1.1314]
+    y = orc.rmsnorm(np.array([3 + 4j]), np.ones(2), eps=0.0)
+    assert abs(y[0].real - 3 / np.sqrt(12.5)) < 1e-15 and abs(y[0].imag - 4 / np.sqrt(12.5)) < 1e-15
+    assert abs(y[0].real - 0.8485) < 1e-4 and abs(y[0].imag - 1.1314) < 1e-4
+    # all ones, eps -> 0: unit RMS; gamma = 0 -> 0
+    assert np.allclose(orc.rmsnorm(np.ones(8) * (1 + 1j), np.ones(16), 0.0), 1 + 1j)
+    assert not orc.rmsnorm(np.arange(1, 5) * (1 - 2j), np.zeros(8)).any()
+    # gamma applies per real component: re and im of one column get their own weights
+    y = orc.rmsnorm(np.array([1 + 1j]), np.array([2.0, 0.5]), 0.0)
+    assert np.isclose(y[0], 2 + 0.5j)
+
+
+def test_silu_spec_examples():
+    # silu(0) = 0, silu(1) = 1/(1+e^-1) = 0.7311, large x -> x
+    assert orc.silu(0.0) == 0.0
+    assert abs(orc.silu(1.0) - 1 / (1 + np.exp(-1.0))) < 1e-16 and abs(orc.silu(1.0) - 0.7311) < 1e-4
+    assert abs(orc.silu(40.0) - 40.0) < 1e-12 and abs(orc.silu(-40.0)) < 1e-15
+    z = orc.silu_c(np.array([1 - 1j]))
+    assert np.isclose(z[0], orc.silu(1.0) + 1j * orc.silu(-1.0))
+
+
+def test_block_zero_weights_is_identity():
+    # all-zero weights -> output = x (residual-only path); every GEMV gives 0
+    m, dff = 32, 48
+    zero = {p: (np.zeros((n, mm), complex), np.zeros((n, mm), complex))
+            for p, n, mm in (("q", m, m), ("k", m, m), ("v", m, m), ("o", m, m),
+                             ("gate", dff, m), ("up", dff, m), ("down", m, dff))}
+    h = wi.activations(5, m)[0].astype(np.complex128)
+    g = (np.ones(2 * m), np.ones(2 * m))
+    out, mid = orc.block_forward(zero, h, g)
+    assert np.array_equal(out, h) and not mid["v"].any() and not mid["act"].any()
+
+
+def test_block_identity_projections_closed_form():
+    # U_re = I for every projection (scales 1, W = 0): q = k = v = rmsnorm(h), h1 = h + v,
+    # gate = up = rmsnorm(h1), a = silu(gate) (.) up, h2 = h1 + a -- each step by hand
+    m = 16
+    eye = np.zeros((4, m, m), np.int8)
+    eye[0] = np.eye(m, dtype=np.int8)
+    U, Wd = orc.build_dense(orc.pack_planar(eye), m, m, np.ones(4, np.float32))
+    assert np.array_equal(U, np.eye(m)) and not Wd.any()
+    layer = {p: (U, Wd) for p in ("q", "k", "v", "o", "gate", "up", "down")}
+    h = wi.activations(6, m)[0].astype(np.complex128)
+    g1 = wi.scales(7, m // 2, True, 0.5, 1.5).reshape(-1).astype(np.float64)
+    g2 = wi.scales(8, m // 2, True, 0.5, 1.5).reshape(-1).astype(np.float64)
+    out, mid = orc.block_forward(layer, h, (g1, g2), eps=1e-5)
+    v = np.stack([h.real, h.imag], -1).reshape(-1)
+    xa = v * g1 / np.sqrt(np.mean(v * v) + 1e-5)
+    h1 = h + (xa[0::2] + 1j * xa[1::2])
+    w = np.stack([h1.real, h1.imag], -1).reshape(-1)
+    xm = w * g2 / np.sqrt(np.mean(w * w) + 1e-5)
+    act = xm / (1 + np.exp(-xm)) * xm
+    want = h1 + (act[0::2] + 1j * act[1::2])
+    assert np.allclose(mid["h1"], h1, rtol=1e-14, atol=1e-14)
+    assert np.allclose(out, want, rtol=1e-14, atol=1e-14)
