@@ -58,7 +58,17 @@ struct ProgParams {
     int32_t nstages, world, rank_base, ranks_in_launch, ctas_per_rank;
     int32_t nslot, slot_bytes, x_bytes, has_mul;
     int32_t off_ring, off_scratch, off_part, off_bars;
+    unsigned long long* trace;  // tools only (ww_debug_program_trace): per CTA and stage,
+                                // globaltimer at [start, polled, x ready, rows done, producer]
 };
+
+__device__ __forceinline__ void ptrace(const ProgParams& p, int s, int ev) {
+    if (p.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[((size_t)blockIdx.x * p.nstages + s) * 8 + ev] = t;
+    }
+}
 
 // ------------------------------------------------------------------ PTX helpers (program only)
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -93,6 +103,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void red_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -102,6 +120,12 @@ __device__ __forceinline__ float2 ldcg2(const float* p) {  // L2 only: written b
     return v;
 }
 __device__ __forceinline__ float silu(float v) { return v / (1.0f + expf(-v)); }
+
+// whole rows of a stage packed into one ring slot (one bulk copy, one full/empty pair)
+__host__ __device__ __forceinline__ int rows_per_slot(int slot_bytes, int row_bytes) {
+    const int r = slot_bytes / row_bytes;
+    return r < 1 ? 1 : r;
+}
 
 // per-warp contiguous row range [w0, w1) of a CTA's NRc rows (sizes differ by <= 1, the
 // longer ranges on the first warps: equal work per SM sub-partition, +-1 row)
@@ -153,20 +177,26 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
                 const int NRc = (int)(r1 - r0);
                 const int ub = NRc / kCW, ue = NRc - ub * kCW;
                 const uint32_t rb = (uint32_t)(16 * D.W);
+                const int rps = rows_per_slot(p.slot_bytes, (int)rb);
+                const int U0 = (ub + rps - 1) / rps, U1 = (ub + rps) / rps;  // units per warp
                 const uint4* src0 = D.packed + r0 * D.W;
-                for (int q = 0; q <= ub; ++q) {
-                    const int nw = q < ub ? kCW : ue;
-                    for (int w = 0; w < nw; ++w) {
-                        const int r = w * ub + (w < ue ? w : ue) + q;
+                for (int u = 0; u < (ue ? U1 : U0); ++u) {
+                    for (int w = 0; w < kCW; ++w) {
+                        const int nr = ub + (w < ue ? 1 : 0);  // the warp's rows
+                        if (u * rps >= nr) break;  // warps holding unit u are a prefix
+                        const int q0 = u * rps;
+                        const int cnt = nr - q0 < rps ? nr - q0 : rps;
+                        const int r = w * ub + (w < ue ? w : ue) + q0;
                         const int k = (int)(seq % (uint32_t)p.nslot);
-                        const uint32_t u = seq / (uint32_t)p.nslot;
-                        if (u > 0) mbar_wait(bars + 8u * (p.nslot + k), (u - 1) & 1);
-                        mbar_expect_tx(bars + 8u * k, rb);
-                        bulk_g2s(ring + (uint32_t)k * p.slot_bytes, src0 + (int64_t)r * D.W, rb,
-                                 bars + 8u * k);
+                        const uint32_t use = seq / (uint32_t)p.nslot;
+                        if (use > 0) mbar_wait(bars + 8u * (p.nslot + k), (use - 1) & 1);
+                        mbar_expect_tx(bars + 8u * k, rb * (uint32_t)cnt);
+                        bulk_g2s(ring + (uint32_t)k * p.slot_bytes, src0 + (int64_t)r * D.W,
+                                 rb * (uint32_t)cnt, bars + 8u * k);
                         ++seq;
                     }
                 }
+                ptrace(p, s, 4);
             }
         }
         return;
@@ -189,17 +219,26 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
         warp_rows(NRc, warp, w0, w1);
 
         // ---- readiness: stage s reads what stage s-1 wrote on every rank
+        if (threadIdx.x == 0) ptrace(p, s, 0);
         if (s > 0) {
             bar_consumers();  // this CTA's rows of stage s-1 are stored
             if (threadIdx.x == 0) {
-                __threadfence_system();
-                for (int g = 0; g < p.world; ++g) red_release_sys(p.sync[g], 1u);
+                // release (cumulative over the CTA's stores ordered before bar.sync): GPU
+                // scope on one GPU, system scope when peers read the stored rows
+                if (p.world == 1)
+                    red_release_gpu(p.sync[0], 1u);
+                else
+                    for (int g = 0; g < p.world; ++g) red_release_sys(p.sync[g], 1u);
             }
         }
         if (D.wait && threadIdx.x == 0) {
             const uint32_t target = epoch * (uint32_t)(p.nstages - 1) * T + (uint32_t)s * T;
-            while ((int32_t)(ld_acquire_sys(my_sync) - target) < 0) __nanosleep(64);
+            if (p.world == 1)
+                while ((int32_t)(ld_acquire_gpu(my_sync) - target) < 0) __nanosleep(32);
+            else
+                while ((int32_t)(ld_acquire_sys(my_sync) - target) < 0) __nanosleep(32);
         }
+        if (threadIdx.x == 0) ptrace(p, s, 1);
         bar_consumers();
         // ---- x (and the second operand) by TMA into the swizzled x regions
         if (threadIdx.x == 0) {
@@ -213,6 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
         }
         mbar_wait(xbar, xphase);
         xphase ^= 1u;
+        if (threadIdx.x == 0) ptrace(p, s, 2);
+        // (event 3: prologue done, below)
         // ---- fused prologue ops on the staged x (granule gi = 16 B = 2 complex columns)
         if (pro != WW_PRO_NONE) {
             const int ng = 8 * 32 * J;
@@ -251,19 +292,44 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
             bar_consumers();
         }
 
-        // ---- the warp's rows: weights from the ring, x from shared memory
+        // ---- the warp's rows, in units of up to rps consecutive rows per ring slot:
+        // weights from the ring, x from shared memory.  The stage's fields are copied to
+        // registers once (the mbarrier asm clobbers memory: no reloads in the row loop).
+        const uint32_t rb = (uint32_t)(16 * D.W);
+        const int rps = rows_per_slot(p.slot_bytes, (int)rb);
+        const float* const scl = D.scales + (D.per_row ? 4 * r0 : 0);
+        const int sstep = D.per_row ? 4 : 0;
+        const float* const resid = D.residual;
+        const int conv = D.conv, ndst = D.ndst;
+        const int64_t grow0 = D.row0 + r0, silu_rows = D.silu_rows;
+        float2* const ydst0 = reinterpret_cast<float2*>(D.ydst[0]);
+        unsigned long long waited = 0;
+        int j = rps;  // row within the current unit (rps: start a new unit)
+        uint32_t useq = seq_base + (uint32_t)warp - kCW, slot = 0;
         for (int r = w0; r < w1; ++r) {
-            const uint32_t seq = seq_base + (uint32_t)(r - w0) * kCW + (uint32_t)warp;
-            const int k = (int)(seq % (uint32_t)p.nslot);
-            const int64_t grow = D.row0 + r0 + r;  // global row index of the stage
+            if (j == rps) {  // next unit: its ring slot, wait until the bulk copy landed
+                j = 0;
+                useq += kCW;
+                const uint32_t k = useq % (uint32_t)p.nslot;
+                slot = k;
+                unsigned long long t0 = 0;
+                if (p.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                mbar_wait(bars + 8u * k, (useq / (uint32_t)p.nslot) & 1);
+                if (p.trace) {
+                    unsigned long long t1;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                    waited += t1 - t0;
+                }
+            }
+            const bool last_in_unit = j == rps - 1 || r == w1 - 1;
+            const int64_t grow = grow0 + r;  // global row index of the stage
             float4 sc = make_float4(0.f, 0.f, 0.f, 0.f);
             float2 res = make_float2(0.f, 0.f);
             if (lane == 0) {  // row operands of the epilogue, fetched a row ahead of use
-                sc = __ldg(reinterpret_cast<const float4*>(D.scales + (D.per_row ? 4 * (r0 + r) : 0)));
-                if (epi == WW_EPI_RESIDUAL) res = ldcg2(D.residual + 2 * grow);
+                sc = __ldg(reinterpret_cast<const float4*>(scl + sstep * r));
+                if (epi == WW_EPI_RESIDUAL) res = ldcg2(resid + 2 * grow);
             }
-            mbar_wait(bars + 8u * k, (seq / (uint32_t)p.nslot) & 1);
-            const uint32_t wl = ring + (uint32_t)k * p.slot_bytes + (uint32_t)lane * 16u;
+            const uint32_t wl = ring + slot * (uint32_t)p.slot_bytes + (uint32_t)j * rb + (uint32_t)lane * 16u;
             uint32_t xc = xl;
             uint4 cur = lds128u(wl);
 #pragma unroll 1
@@ -274,7 +340,8 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
                 xc += 4096u;
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(bars + 8u * (p.nslot + k));  // slot free
+            if (last_in_unit && lane == 0) mbar_arrive(bars + 8u * (p.nslot + slot));  // free
+            ++j;
             reduce_to<1>(acc, scratch);
             acc.zero();
             if (lane == 0) {
@@ -282,21 +349,30 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
 #pragma unroll
                 for (int i = 0; i < 8; ++i) Tt[i] = scratch[i];
                 float yre = sc.x * Tt[0] - sc.y * Tt[3] + sc.z * Tt[4] + sc.w * Tt[7];  // Eq. 2
-                float yim = D.conv == WW_CONV_EQ1
+                float yim = conv == WW_CONV_EQ1
                                 ? sc.x * Tt[1] + sc.y * Tt[2] - sc.z * Tt[5] + sc.w * Tt[6]   // Eq. 1
                                 : sc.x * Tt[1] + sc.y * Tt[2] + sc.z * Tt[5] - sc.w * Tt[6];  // Eq. 3
                 if (epi == WW_EPI_RESIDUAL) {
                     yre = yre + res.x;
                     yim = yim + res.y;
-                } else if (epi == WW_EPI_SILU && grow < D.silu_rows) {
+                } else if (epi == WW_EPI_SILU && grow < silu_rows) {
                     yre = silu(yre);
                     yim = silu(yim);
                 }
-                for (int g = 0; g < D.ndst; ++g)
-                    reinterpret_cast<float2*>(D.ydst[g])[grow] = make_float2(yre, yim);
+                ydst0[grow] = make_float2(yre, yim);
+                for (int g = 1; g < ndst; ++g)
+                    reinterpret_cast<float2*>(SD[s].ydst[g])[grow] = make_float2(yre, yim);
             }
         }
-        seq_base += (uint32_t)NRc;
+        if (warp == 0 && lane == 0 && p.trace)
+            p.trace[((size_t)blockIdx.x * p.nstages + s) * 8 + 3] = waited;  // (replaces event 3)
+        {
+            const int ub = NRc / kCW, ue = NRc - ub * kCW;
+            const int U0 = (ub + rps - 1) / rps, U1 = (ub + rps) / rps;
+            seq_base += (uint32_t)(kCW * U0 + (U1 > U0 ? ue : 0));  // units of the stage
+        }
+        if (lane == 0 && (warp == 0 || warp == 8 || warp == kCW - 1))
+            ptrace(p, s, warp == 0 ? 5 : (warp == 8 ? 7 : 6));
     }
 
     // ---- exit: the last CTA of this rank advances the epoch for the next launch
@@ -313,6 +389,13 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
 }  // namespace
 
 // ---------------------------------------------------------------------------- host side
+static unsigned long long* g_prog_trace = nullptr;  // tools only
+// Not part of the ABI (no declaration in ww.h): tools/prog_trace.py points the program kernel
+// at a device buffer of grid x nstages x 8 u64 globaltimer stamps (NULL: off, the default).
+extern "C" void ww_debug_program_trace(void* dev_buf) {
+    g_prog_trace = reinterpret_cast<unsigned long long*>(dev_buf);
+}
+
 static_assert(sizeof(StageDev) % 128 == 0, "descriptor alignment");
 
 extern "C" size_t ww_program_workspace_bytes(int32_t nstages, int32_t ranks_in_launch) {
@@ -452,6 +535,7 @@ extern "C" ww_status ww_program_run(const ww_program* P, void* stream) {
     p.off_scratch = p.off_ring + P->nslot * P->slot_bytes + 512;
     p.off_part = p.off_scratch + kCW * 8 * 4;
     p.off_bars = (p.off_part + 32 * 4 + 7) / 8 * 8;
+    p.trace = g_prog_trace;
     const int pe = ww::prepare_kernel(reinterpret_cast<const void*>(wl_program_kernel), kSmemMax);
     if (pe) return ww::fail(WW_ERR_CUDA, "%s: %s", fn, cudaGetErrorString((cudaError_t)pe));
     cudaLaunchConfig_t cfg = {};
