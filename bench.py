@@ -192,7 +192,33 @@ def cpu_baseline(seed=0, runs=3) -> dict:
     return {"value": allc["value"], "unit": "GB/s", "cores": allc["cores"], "kind": "oracle",
             "sample": SAMPLE + f"; median of {runs} runs; value = OpenMP over rows on all "
                       "usable cores (`single` = one thread)",
-            "single_thread": out["single"], "all_cores": allc, **host_info()}
+            "single_thread": out["single"], "all_cores": allc,
+            "paper_alg1_avx512": alg1_baseline(work, runs), **host_info()}
+
+
+def alg1_baseline(work, runs=3) -> dict:
+    """The paper's own CPU kernel (Algorithm 1, AVX-512F + BMI2, OpenMP rows; NEXT-4) on the
+    same sample: a like-for-like CPU datapath beside the oracle.  GB/s of packed weights."""
+    try:
+        import cpu_alg1
+        if not cpu_alg1.supported():
+            return {"unavailable": "host CPU lacks AVX-512F or BMI2"}
+    except OSError as e:
+        return {"unavailable": f"libww_cpu.so: {e}"}
+    out = {}
+    for name, T in (("single", 1), ("all_cores", 0)):
+        ts = []
+        for _ in range(runs + 1):  # first pass warms the pages
+            t0 = time.perf_counter()
+            nb = 0
+            for planar, nr, m, sc, x in work:
+                cpu_alg1.wl_gemv(planar, nr, m, sc, x, 0, T)
+                nb += 16 * nr * ((m + 15) // 16)
+            ts.append(time.perf_counter() - t0)
+        t = float(np.median(ts[1:]))
+        out[name] = {"value": round(nb / t / 1e9, 4), "unit": "GB/s", "ms_per_layer": round(1e3 * t, 3),
+                     "cores": 1 if T == 1 else cpu_alg1.max_threads()}
+    return out
 
 
 def run_reference(args, world, rank):

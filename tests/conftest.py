@@ -20,6 +20,7 @@ def _built():
     import build  # noqa: E402
 
     build.build_oracle()
+    build.build_cpu_alg1()
     build.build_inputs()
     if any(f.endswith((".cu", ".cc")) for f in os.listdir(build.CSRC)):
         build.build_product()

@@ -110,8 +110,20 @@ def build_variant(name, defines):
     return out
 
 
+def build_cpu_alg1(force=False):
+    """cpu_alg1/libww_cpu.so: the paper's AVX-512 + BMI2 Algorithm 1 (NEXT-4 CPU baseline).
+    Compiled for x86-64 with the AVX-512 code in target-attributed functions (runtime check)."""
+    d = os.path.join(ROOT, "cpu_alg1")
+    out = os.path.join(d, "libww_cpu.so")
+    srcs = [os.path.join(d, "ww_cpu.c"), os.path.join(d, "ww_cpu.h")]
+    if force or _stale(out, srcs):
+        _run(["gcc", "-std=c11", "-O3", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+              "-Wall", "-o", out, srcs[0]])
+
+
 def build_all(force=False):
     build_oracle(force)
+    build_cpu_alg1(force)
     build_inputs(force)
     build_product(force)
 
