@@ -145,8 +145,46 @@ struct Acc {
 
 // One column (8 code bits = 4 planes) against one activation pair: Eq. 6 (bit 2p+1, add)
 // and Eq. 7 (bit 2p, subtract) for each plane p.
+// NEXT-2 ablation switches (tools/ablation_o1o4.py builds each as a separate library; all 0
+// in the product): WW_ABL_NO_O1 -- no mask reuse, the real and the imaginary path decode
+// their own predicates and add with scalar FADDs; WW_ABL_NO_O2 -- no input reuse, every
+// plane re-loads its (x_re, x_im) pair from shared memory; WW_ABL_NO_O4 -- no register-
+// resident accumulators, they are spilled to local memory and reloaded after every chunk.
+#ifndef WW_ABL_NO_O1
+#define WW_ABL_NO_O1 0
+#endif
+#ifndef WW_ABL_NO_O2
+#define WW_ABL_NO_O2 0
+#endif
+#ifndef WW_ABL_NO_O4
+#define WW_ABL_NO_O4 0
+#endif
+
+__device__ __forceinline__ float2 lds64v(uint32_t addr) {  // a load ptxas cannot merge
+    float2 v;
+    asm volatile("ld.volatile.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
 template <int N>
-__device__ __forceinline__ void column(float2 (&pos)[4], float2 (&neg)[4], uint32_t bits, float2 x) {
+__device__ __forceinline__ void column(float2 (&pos)[4], float2 (&neg)[4], uint32_t bits, float2 x,
+                                       uint32_t bits_im = 0) {
+#if WW_ABL_NO_O1
+    // each path decodes its own predicates (two R2P + tests per column, bits_im extracted
+    // from the code word by a second, different instruction so ptxas cannot share them)
+    // and adds alone
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int q = k >> 1;
+        if (bits & (1u << k)) pos[q].x = __fadd_rn(pos[q].x, (k & 1) ? x.x : -x.x);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int q = k >> 1;
+        if (bits_im & (1u << k)) pos[q].y = __fadd_rn(pos[q].y, (k & 1) ? x.y : -x.y);
+    }
+    return;
+#endif
     const float2 nx = make_float2(-x.x, -x.y);
     // bits in ascending order (bit 2q = -1 of plane q, bit 2q+1 = +1) so the compiler can
     // turn a column's 8 predicates into one R2P of bits 0..6 plus one bit test
@@ -176,15 +214,64 @@ __device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xl, u
         const uint32_t sh = (kk & 1) * 16;
         const uint32_t bits_a = (word >> sh) & 0xffu, bits_b = (word >> (sh + 8)) & 0xffu;
         const uint32_t xa = xl ^ ((uint32_t)kk << 4);
+#if WW_ABL_NO_O2
+        if (B == 1) {  // every plane re-loads x: 4 loads per column instead of one per pair
+#pragma unroll
+            for (int c = 1; c >= 0; --c) {
+                const uint32_t bits = c ? bits_b : bits_a;
+                float2(&pos)[4] = acc.a[c ? S - 1 : 0][0][0];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 x = lds64v(xa + 8u * c);
+                    if (bits & (2u << (2 * q))) pos[q] = fadd2(pos[q], x);
+                    if (bits & (1u << (2 * q))) pos[q] = fadd2(pos[q], make_float2(-x.x, -x.y));
+                }
+            }
+            continue;
+        }
+#endif
 #pragma unroll
         for (int b = 0; b < B; ++b) {  // each decoded code drives all B vectors (a9)
             const float4 v = lds128(xa + b * bstride);
             // (odd column first: the same sums -- each column-parity set keeps its own
             // order -- but ptxas then needs no predicate spill across the R2Ps)
+#if WW_ABL_NO_O1
+            // the same bytes through PRMT (byte select), a second decode path
+            const uint32_t ia = __byte_perm(word, 0u, 0x4440u | (2u * (kk & 1))),
+                           ib = __byte_perm(word, 0u, 0x4440u | (2u * (kk & 1) + 1u));
+            column<N>(acc.a[S - 1][0][b], acc.a[S - 1][N - 1][b], bits_b, make_float2(v.z, v.w), ib);
+            column<N>(acc.a[0][0][b], acc.a[0][N - 1][b], bits_a, make_float2(v.x, v.y), ia);
+#else
             column<N>(acc.a[S - 1][0][b], acc.a[S - 1][N - 1][b], bits_b, make_float2(v.z, v.w));
             column<N>(acc.a[0][0][b], acc.a[0][N - 1][b], bits_a, make_float2(v.x, v.y));
+#endif
         }
     }
+#if WW_ABL_NO_O4
+    {  // accumulators leave the registers after every chunk: spill to local memory, reload
+        volatile float2 spill[S][N][B][4];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int k = 0; k < N; ++k)
+#pragma unroll
+                for (int b = 0; b < B; ++b)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        spill[s][k][b][q].x = acc.a[s][k][b][q].x;
+                        spill[s][k][b][q].y = acc.a[s][k][b][q].y;
+                    }
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int k = 0; k < N; ++k)
+#pragma unroll
+                for (int b = 0; b < B; ++b)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        acc.a[s][k][b][q] = make_float2(spill[s][k][b][q].x, spill[s][k][b][q].y);
+    }
+#endif
 }
 
 // Transpose-reduce NV (power of 2) partial sums across the warp: after the halving rounds

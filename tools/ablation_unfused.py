@@ -40,7 +40,10 @@ def timed(fn, R, reps=10):
 
 
 def main():
-    print(torch.cuda.get_device_name(), flush=True)
+    js = "--json" in sys.argv
+    out = {}
+    if not js:
+        print(torch.cuda.get_device_name(), flush=True)
     for (n, m) in ((2048, 2048), (5504, 2048), (2048, 5504)):
         nb = ww.packed_bytes(n, m)
         R = max(2, int(np.ceil(4 * L2 / nb)))
@@ -60,9 +63,14 @@ def main():
         Lu = ww.Layer(n, m, ww.LAYOUT_PLANAR, flags=ww.FLAG_PDL)
         fused = timed(lambda r, s: ww.wl_gemv(Lf, Wc[r], sc, X[r], Y[r], stream=s), R)
         unfused = timed(lambda r, s: ww.wl_gemv_unfused(Lu, Wp[r], sc, X[r], Y[r], acc, stream=s), R)
-        print(f"complex {n}x{m}: fused {fused:7.2f} us   unfused 8x real + combine {unfused:7.2f} us"
-              f"   fusion speedup {unfused / fused:.2f}x", flush=True)
+        out[f"{n}x{m}"] = round(unfused, 3)
+        if not js:
+            print(f"complex {n}x{m}: fused {fused:7.2f} us   unfused 8x real + combine "
+                  f"{unfused:7.2f} us   fusion speedup {unfused / fused:.2f}x", flush=True)
         del Wc, Wp
+    if js:
+        import json
+        print(json.dumps(out))
 
 
 if __name__ == "__main__":
