@@ -31,7 +31,86 @@ __device__ __forceinline__ uint32_t ldg_stream32(const uint32_t* p) {
 // acc[i] = sum_j t_ij * xc_j for one plane of the App. H planar layout (n x W words, slot k
 // of word c = column 16c+k, bit 2k+1 = +1, bit 2k = -1) and one real component
 // xc of the complex64 vector x (Eqs. 6-7: +1 adds, -1 subtracts, 0 / (1,1) contribute 0).
-// A warp owns a row (rows round-robin over the CTA's 16 warps), lanes take 16-column words,
+// Tuned like the fused kernel: a warp owns a row (contiguous per-warp row ranges), each lane
+// streams one 128-bit load = 4 words = 64 consecutive columns per sweep (2048 columns per
+// warp sweep, two sweeps in flight), predicated fp32 adds (R2P-decoded), x staged once per
+// CTA with the lane blocks' 16 granules XOR-swizzled (granule g of 64-column block L at
+// L*16 + (g ^ (L & 15))) so the 32 lanes' LDS.128 are conflict-free; the rows' four
+// accumulators reduced by warp shuffles.  Needs a 16-B aligned plane (W % 4 == 0: 64 | m);
+// other shapes take the word-per-lane kernel below.
+__global__ void __launch_bounds__(kWarps * 32, 2)
+tern_plane_v4_kernel(const uint32_t* __restrict__ plane, const float* __restrict__ X, int comp,
+                     int64_t n, int64_t m, int64_t W, float* __restrict__ acc_out) {
+    extern __shared__ __align__(16) float xs4[];  // nblk x 16 granules x 4 floats
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * n / gridDim.x;
+    const int64_t r1 = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
+    const int NRc = (int)(r1 - r0);
+    const int ub = NRc / kWarps, ue = NRc - ub * kWarps;
+    const int w0 = warp * ub + (warp < ue ? warp : ue), w1 = w0 + ub + (warp < ue ? 1 : 0);
+    const int64_t W4 = W / 4;             // 64-column blocks per row
+    const int J = (int)((W4 + 31) / 32);  // sweeps per row
+    pdl_launch_dependents();
+    const uint4* base = reinterpret_cast<const uint4*>(plane) + (r0 + w0) * W4 + lane;
+    int pr = w0, pk = 0;
+    auto load_next = [&]() -> uint4 {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        const int64_t blk = (int64_t)pk * 32 + lane;
+        if (pr < w1 && blk < W4)
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "l"(base + (int64_t)(pr - w0) * W4 + (int64_t)pk * 32));
+        if (++pk == J) {
+            pk = 0;
+            ++pr;
+        }
+        return v;
+    };
+    uint4 qa = load_next(), qb = load_next();
+    pdl_wait();
+    const int64_t nblk = (int64_t)J * 32;
+    for (int64_t e = threadIdx.x; e < nblk * 16; e += blockDim.x) {  // stage xc, swizzled
+        const int64_t L = e >> 4, g = e & 15;
+        float4 v;
+        float* vp = &v.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t col = L * 64 + g * 4 + q;
+            vp[q] = col < m ? X[2 * col + comp] : 0.f;
+        }
+        reinterpret_cast<float4*>(xs4)[L * 16 + (g ^ (L & 15))] = v;
+    }
+    __syncthreads();
+    for (int r = w0; r < w1; ++r) {
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int k = 0; k < J; ++k) {
+            const uint4 w = qa;
+            qa = qb;
+            qb = load_next();
+            const int64_t L = (int64_t)k * 32 + lane;
+            const float4* xb = reinterpret_cast<const float4*>(xs4) + L * 16;
+            const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int g = 0; g < 16; ++g) {
+                const float4 v = xb[g ^ (int)(L & 15)];
+                const float xv[4] = {v.x, v.y, v.z, v.w};
+                const uint32_t word = w4[g >> 2];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int slot = 4 * (g & 3) + q;
+                    if (word & (2u << (2 * slot))) a[q] = __fadd_rn(a[q], xv[q]);
+                    if (word & (1u << (2 * slot))) a[q] = __fadd_rn(a[q], -xv[q]);
+                }
+            }
+        }
+        float t = (a[0] + a[1]) + (a[2] + a[3]);
+#pragma unroll
+        for (int off = 16; off; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (lane == 0) acc_out[r0 + r] = t;
+    }
+}
+
+// Word-per-lane variant (any m): a warp owns a row (rows round-robin over the CTA's 16 warps), lanes take 16-column words,
 // 32 words per sweep; x is staged once per CTA transposed by granule (granule g of word c at
 // (g*Wp + c)*16) so 32 lanes reading their words' granule g hit consecutive addresses.
 __global__ void __launch_bounds__(kWarps * 32, 2)
@@ -171,6 +250,23 @@ extern "C" ww_status ww_ternary_gemv_plane(int64_t n, int64_t m, const void* pla
     }
     const uint32_t* pl = reinterpret_cast<const uint32_t*>(planar_d) + (int64_t)plane * n * W;
     const int grid = (int)std::min<int64_t>(sm_count(), n);
+    if (W % 4 == 0 && ((uintptr_t)planar_d & 15) == 0) {  // the 128-bit kernel
+        const int64_t J = (W / 4 + 31) / 32;
+        const size_t smem4 = (size_t)J * 32 * 16 * 16;
+        if (smem4 <= 200 * 1024) {
+            const int e4 = ww::prepare_kernel(reinterpret_cast<const void*>(tern_plane_v4_kernel),
+                                              200 * 1024);
+            if (e4)
+                return ww::fail(WW_ERR_CUDA, "ww_ternary_gemv_plane: %s",
+                                cudaGetErrorString((cudaError_t)e4));
+            cudaError_t e = launch_pdl(tern_plane_v4_kernel, dim3(grid), dim3(kWarps * 32), smem4,
+                                       (cudaStream_t)stream, (flags & WW_FLAG_PDL) != 0, pl, x_d,
+                                       (int)comp, n, m, W, acc_d);
+            if (e != cudaSuccess)
+                return ww::fail(WW_ERR_CUDA, "ww_ternary_gemv_plane: %s", cudaGetErrorString(e));
+            return ww::ok();
+        }
+    }
     cudaError_t e = launch_pdl(tern_plane_kernel, dim3(grid), dim3(kWarps * 32), smem,
                                (cudaStream_t)stream, (flags & WW_FLAG_PDL) != 0, pl, x_d, (int)comp,
                                n, m, W, acc_d);
