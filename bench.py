@@ -267,13 +267,17 @@ def run_ours(args, world, rank, local):
     group = dist.group.WORLD if world > 1 else None
 
     if args.workload == "c4":
+        gam = None
+        if args.chain == "block":
+            from paper_2604_20913_b200.stack import block_gammas
+            gam = [tuple(torch.from_numpy(g).to(dev) for g in pair)
+                   for pair in block_gammas(args.seed, args.layers, 2048)]
         base = WLStack(layers=args.layers, seed=args.seed, B=args.batch, rank=rank, world=world,
-                       pdl=not args.no_pdl, device=dev, group=group, fuse=not args.no_fuse)
+                       pdl=not args.no_pdl, device=dev, group=group, fuse=not args.no_fuse,
+                       chain=args.chain if args.engine == "pdl" else "plain", gammas=gam)
         if args.engine == "program":
-            stack = ProgramRunner(base, args.chain, args.seed)
+            stack = ProgramRunner(base, args.chain, gam)
         else:
-            if args.chain != "plain":
-                raise SystemExit("--chain block needs --engine program")
             stack = base
         units = [stack]
         layers_per_step = 7 * args.layers  # widely-linear projections per token
@@ -512,7 +516,7 @@ def _e2e(stack, args, s, dev, graph, world, alg_bytes):
     -> HBM each step, the last projection's gathered output -> host each step."""
     import torch
     import torch.distributed as dist
-    xflat = (stack.inputs() if hasattr(stack, "inputs") else stack.X).view(-1)
+    xflat = stack.inputs().view(-1)
     xh = torch.empty(xflat.numel(), dtype=torch.complex64).pin_memory()
     xh.copy_(xflat.cpu())
     last = stack.Y[-1]
@@ -559,19 +563,13 @@ class ProgramRunner:
     """The C4 stack as ONE persistent program launch per token (ww_program_run): the same
     weights, scales and gathered outputs as the per-launch WLStack."""
 
-    def __init__(self, base, chain, seed):
-        import torch
+    def __init__(self, base, chain, gam):
         import paper_2604_20913_b200 as ww
-        from paper_2604_20913_b200.stack import block_gammas, program_stages
+        from paper_2604_20913_b200.stack import program_stages
         if base.world != 1:
             raise SystemExit("--engine program at world > 1 needs peer-mapped outputs (not wired "
                              "in bench.py); use the default engine")
-        self.base, self.chain = base, chain
-        gam = None
-        if chain == "block":
-            gam = [tuple(torch.from_numpy(g).to(base.device) for g in pair)
-                   for pair in block_gammas(seed, base.layers, 2048)]
-        self.gam = gam
+        self.base, self.chain, self.gam = base, chain, gam
         self.prog = ww.Program([program_stages(base, [base], chain, gam)], world=1)
         self.stages, self.X, self.Y = base.stages, base.X, base.Y
 
@@ -621,6 +619,9 @@ class _ReplicaLayer:
         self.L = ww.Layer(self.nloc, spec.m, ww.LAYOUT_COL4,
                           ww.SCALES_PER_ROW if spec.per_row else ww.SCALES_PER_TENSOR,
                           ww.CONV_EQ1, 0 if args.no_pdl else ww.FLAG_PDL)
+
+    def inputs(self):
+        return self.X
 
     def step(self, s):
         rpr = self.shard.rows_per_rank

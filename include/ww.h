@@ -199,6 +199,24 @@ ww_status ww_wl_combine(const ww_layer* L, const float* acc8_d, const float* sca
 #define WW_EPI_RESIDUAL 1
 #define WW_EPI_SILU 2
 
+/* Per-stage kernel with the same fused decode-block ops (B = 1, x of one shared-memory tile,
+ * 16 | m, TMA staging): WW_PRO_* on the staged x before the sweep, WW_EPI_* on each output
+ * row.  residual is indexed by row0 + local row (the global row of a row-sharded stage);
+ * silu_rows compares against the same global index.  ops == NULL is ww_wl_gemv.  Errors:
+ * WW_ERR_MISALIGNED (16-B x / x2 / gamma, 8-B residual / y), WW_ERR_UNSUPPORTED (x and x2
+ * beyond shared memory), WW_ERR_INVALID_ARGUMENT (missing operand, x / y overlap). */
+typedef struct {
+    int32_t prologue, epilogue; /* WW_PRO_*, WW_EPI_* */
+    const float* x2;            /* WW_PRO_MUL: second complex64[m] operand */
+    const float* gamma;         /* WW_PRO_RMSNORM: 2m fp32 */
+    float eps;
+    const float* residual;      /* WW_EPI_RESIDUAL: complex64 by global row */
+    int64_t row0;               /* global index of local row 0 */
+    int64_t silu_rows;          /* WW_EPI_SILU: global rows below get SiLU */
+} ww_ops;
+ww_status ww_wl_gemv_fused(const ww_layer* L, const void* packed_d, const float* scales_d,
+                           const float* x_d, float* y_d, const ww_ops* ops, void* stream);
+
 typedef struct {
     const void* packed;   /* this rank's WW_LAYOUT_COL4 rows [row0, row0 + n_local) */
     const float* scales;  /* their scales: n_local x 4 (per row) or 4 (per tensor) */

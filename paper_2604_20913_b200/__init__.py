@@ -42,7 +42,7 @@ EPI_NONE, EPI_RESIDUAL, EPI_SILU = 0, 1, 2
 EXPORTS = ("ww_packed_bytes", "ww_pack_ternary", "ww_unpack_ternary", "ww_repack",
            "ww_pack_ternary_device", "ww_wl_gemv", "ww_wl_gemv_batched", "ww_shard_plan",
            "ww_query_launch", "ww_status_string", "ww_last_error", "ww_version",
-           "ww_ternary_gemv_plane", "ww_wl_combine", "ww_program_workspace_bytes",
+           "ww_ternary_gemv_plane", "ww_wl_combine", "ww_wl_gemv_fused", "ww_program_workspace_bytes",
            "ww_program_sync_bytes", "ww_program_init", "ww_program_run")
 
 
@@ -89,6 +89,13 @@ class _Program(ctypes.Structure):
         ("workspace", ctypes.c_void_p), ("sync", ctypes.c_void_p * PROG_MAX_RANKS)]
 
 
+class _Ops(ctypes.Structure):
+    _fields_ = [("prologue", ctypes.c_int32), ("epilogue", ctypes.c_int32),
+                ("x2", ctypes.c_void_p), ("gamma", ctypes.c_void_p), ("eps", ctypes.c_float),
+                ("residual", ctypes.c_void_p), ("row0", ctypes.c_int64),
+                ("silu_rows", ctypes.c_int64)]
+
+
 _i64, _i32, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
 _lib.ww_packed_bytes.restype = ctypes.c_size_t
 _lib.ww_packed_bytes.argtypes = [_i64, _i64]
@@ -113,6 +120,9 @@ _lib.ww_ternary_gemv_plane.restype = _i32
 _lib.ww_ternary_gemv_plane.argtypes = [_i64, _i64, _vp, _i32, _vp, _i32, _vp, ctypes.c_uint32, _vp]
 _lib.ww_wl_combine.restype = _i32
 _lib.ww_wl_combine.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _vp]
+_lib.ww_wl_gemv_fused.restype = _i32
+_lib.ww_wl_gemv_fused.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _vp, ctypes.POINTER(_Ops),
+                                  _vp]
 _lib.ww_program_workspace_bytes.restype = ctypes.c_size_t
 _lib.ww_program_workspace_bytes.argtypes = [_i32, _i32]
 _lib.ww_program_sync_bytes.restype = ctypes.c_size_t
@@ -249,6 +259,43 @@ def wl_gemv(layer: Layer, packed, scales, x, y=None, stream=None):
     L = layer.c()
     _check(_lib.ww_wl_gemv(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(), x.data_ptr(),
                            y.data_ptr(), _stream_ptr(stream)))
+    return y
+
+
+@dataclass
+class Ops:
+    """ww_ops: fused decode-block ops of ww_wl_gemv_fused (B = 1)."""
+    prologue: int = 0
+    epilogue: int = 0
+    x2: object = None
+    gamma: object = None
+    eps: float = 1e-5
+    residual: object = None
+    row0: int = 0
+    silu_rows: int = 0
+
+    def c(self) -> _Ops:
+        return _Ops(self.prologue, self.epilogue, None if self.x2 is None else self.x2.data_ptr(),
+                    None if self.gamma is None else self.gamma.data_ptr(), self.eps,
+                    None if self.residual is None else self.residual.data_ptr(), self.row0,
+                    self.silu_rows)
+
+
+def wl_gemv_fused(layer: Layer, packed, scales, x, y=None, ops: Ops | None = None, stream=None):
+    """y = epilogue(WL-GEMV(prologue(x))) for one complex64 CUDA vector (ww_wl_gemv_fused)."""
+    import torch
+    if y is None:
+        y = torch.empty(layer.n, dtype=torch.complex64, device=x.device)
+    _check_args(layer, packed, scales, x, y, 1)
+    for name, t, dt in (("x2", ops and ops.x2, torch.complex64), ("gamma", ops and ops.gamma, torch.float32),
+                        ("residual", ops and ops.residual, torch.complex64)):
+        if t is not None and (not t.is_cuda or t.dtype != dt or t.stride(-1) != 1):
+            raise TypeError(f"{name} must be a unit-stride CUDA {dt} tensor")
+    L = layer.c()
+    O = ops.c() if ops is not None else None
+    _check(_lib.ww_wl_gemv_fused(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(), x.data_ptr(),
+                                 y.data_ptr(), ctypes.byref(O) if O is not None else None,
+                                 _stream_ptr(stream)))
     return y
 
 

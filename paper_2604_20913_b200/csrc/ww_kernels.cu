@@ -91,6 +91,13 @@ struct alignas(64) Params {
                           // bits 8..: trace slot (WW_TRACE builds),
                           // 2 = skip the accumulation, 8 = bulk L2 prefetch of the CTA's
                           // weights at kernel start (overhead measurement); 0 in the product
+    // fused decode-block ops (ww_wl_gemv_fused; B = 1, single tile, TMA staging only)
+    int32_t pro, epi;     // WW_PRO_*, WW_EPI_*
+    float eps;
+    const float* gamma;   // WW_PRO_RMSNORM: 2m fp32
+    const float* residual;  // WW_EPI_RESIDUAL: complex64 by global row
+    int64_t silu_rows, row0;  // WW_EPI_SILU bound; global index of local row 0
+    CUtensorMap tmap2;    // WW_PRO_MUL: second operand, staged after x
 };
 
 // cp.async of one 16-byte x granule (columns col, col+1 of vector row `src`), zero-filling
@@ -155,10 +162,12 @@ __device__ __forceinline__ void stage_x_regions_tma(const Params& p, uint32_t xs
     const int J = p.J;
     for (int j = threadIdx.x; j < J; j += blockDim.x) {
         const uint32_t bar = bars + 8 * j;
-        mbar_expect_tx(bar, (uint32_t)(B * 4096));
+        const bool two = B == 1 && p.pro == WW_PRO_MUL;  // + the second operand's slice
+        mbar_expect_tx(bar, (uint32_t)(B * 4096 * (two ? 2 : 1)));
 #pragma unroll 1
         for (int b = 0; b < B; ++b)
             tma_load_3d(xs + (uint32_t)((b * J + j) * 4096), &p.tmap, 0, 32 * j, b, bar);
+        if (two) tma_load_3d(xs + (uint32_t)((J + j) * 4096), &p.tmap2, 0, 32 * j, 0, bar);
     }
 }
 
@@ -172,6 +181,28 @@ __device__ __forceinline__ void store_y(const Params& p, const float (&T)[8], co
                           ? sUr * T[1] + sUi * T[2] - sWr * T[5] + sWi * T[6]   // Eq. 1
                           : sUr * T[1] + sUi * T[2] + sWr * T[5] - sWi * T[6];  // Eq. 3
     reinterpret_cast<float2*>(p.Y)[b * p.ldy + row] = make_float2(yre, yim);
+}
+
+// B = 1 epilogue with a fused op (NEXT-3): residual add, or SiLU of the rows below silu_rows
+// (global row index), after the scales -- the same arithmetic as the program kernel.
+__device__ __forceinline__ void store_y_ops(const Params& p, const float (&T)[8], const float* s,
+                                            int64_t row, float2 res, float rnorm) {
+    const float sUr = s[0], sUi = s[1], sWr = s[2], sWi = s[3];
+    float yre = sUr * T[0] - sUi * T[3] + sWr * T[4] + sWi * T[7];               // Eq. 2
+    float yim = p.conv == WW_CONV_EQ1 ? sUr * T[1] + sUi * T[2] - sWr * T[5] + sWi * T[6]
+                                      : sUr * T[1] + sUi * T[2] + sWr * T[5] - sWi * T[6];
+    if (p.pro == WW_PRO_RMSNORM) {  // the RMSNorm scalar of the prologue (linear map)
+        yre = yre * rnorm;
+        yim = yim * rnorm;
+    }
+    if (p.epi == WW_EPI_RESIDUAL) {
+        yre = yre + res.x;
+        yim = yim + res.y;
+    } else if (p.epi == WW_EPI_SILU && p.row0 + row < p.silu_rows) {
+        yre = silu_f(yre);
+        yim = silu_f(yim);
+    }
+    reinterpret_cast<float2*>(p.Y)[row] = make_float2(yre, yim);
 }
 
 // Multi-tile epilogue: lane b < B takes vector b's totals from the warp scratch T0.
@@ -196,11 +227,12 @@ struct SmemLayout {
 // ([rows][NV] floats), the CTA's row scales and one mbarrier per x slice.
 // Single tile: x_chunks = 32*J per vector; multi-tile: the tile width.
 __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
-                                                  int nbars, int rows) {
+                                                  int nbars, int rows, bool x2 = false) {
     const int64_t nv = next_pow2(8 * B);
     SmemLayout L;
     L.x_bytes = (int64_t)B * x_chunks * 128;
-    L.scratch_off = L.x_bytes;
+    // WW_PRO_MUL: the second operand right after x; then 32 floats of RMSNorm partials
+    L.scratch_off = L.x_bytes * (x2 ? 2 : 1) + 128;
     L.tot_off = L.scratch_off + (single ? 0 : (int64_t)warps * nv * 4);
     L.scale_off = L.tot_off + (single ? (int64_t)rows * nv * 4 : 0);
     // scales: one 16-B slot per CTA row (per-row mode) or per warp (per-tensor mode)
@@ -229,7 +261,8 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     const bool single = p.single != 0;
     const int nbars = single ? p.J : 0;
     const SmemLayout SL = smem_layout(B, single ? 32 * p.J : p.x_stride, nwarps, single, nbars,
-                                      p.rows_cap);
+                                      p.rows_cap, p.pro == WW_PRO_MUL);
+    float* part = reinterpret_cast<float*>(smem + SL.scratch_off - 128);  // [32]
     float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * NV;
     const uint32_t bars = xs + (uint32_t)SL.bar_off;
 
@@ -306,6 +339,10 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             return w;
         };
         float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][NV]
+        float4 gam[kGammaRegs];  // WW_PRO_RMSNORM: this thread's gamma (a weight), pre-wait
+        if (B == 1 && p.pro == WW_PRO_RMSNORM)
+            gamma_prefetch(gam, p.gamma, p.m, J, threadIdx.x, blockDim.x);
+        float rnorm = 1.0f;  // RMSNorm factor, applied in the epilogue
         auto run = [&](auto&& load_next) {
             uint4 qa = load_next(), qb = load_next();
             __syncthreads();  // mbarrier inits visible
@@ -340,11 +377,29 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             const uint32_t l7 = (uint32_t)(lane & 7) << 4;  // swizzle key of the lane's chunks
             const uint32_t xb = (xs + (uint32_t)lane * 128u) | l7;
             const uint32_t bstride = (uint32_t)J * 4096u;
-            if (w0 < w1)  // x slices in before the warp's first sweep
+            if (B == 1 && p.pro != WW_PRO_NONE) {
+                // fused prologue op (ww_sweep.cuh, NEXT-3): the whole CTA waits for x, rewrites
+                // it in place, and only then sweeps
                 for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * j);
+                const int ng = 8 * 32 * J;
+                if (p.pro == WW_PRO_MUL) {
+                    x_mul(xs, xs + (uint32_t)J * 4096u, ng, threadIdx.x, blockDim.x);
+                } else {
+                    const float ss =
+                        x_gamma_sumsq_warp(xs, ng, threadIdx.x, blockDim.x, gam, p.gamma, p.m);
+                    if (lane == 0) part[warp] = ss;
+                }
+                __syncthreads();
+                if (p.pro == WW_PRO_RMSNORM) rnorm = rms_factor(part, nwarps, p.m, p.eps);
+            } else if (w0 < w1) {  // x slices in before the warp's first sweep
+                for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * j);
+            }
 #pragma unroll 1
             for (int r = w0; r < w1; ++r) {
                 uint32_t xc = xb;
+                float2 res = make_float2(0.f, 0.f);  // WW_EPI_RESIDUAL operand, a row ahead
+                if (B == 1 && p.epi == WW_EPI_RESIDUAL && lane == 0)
+                    res = __ldcg(reinterpret_cast<const float2*>(p.residual) + p.row0 + r0 + r);
 #pragma unroll 1
                 for (int k = 0; k < J; ++k) {
                     const uint4 cur = qa;
@@ -372,7 +427,10 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                     for (int i = 0; i < 8; ++i) T[i] = tot[r * NV + 8 * lane + i];
                     const float* sr = reinterpret_cast<const float*>(smem + SL.scale_off) +
                                       4 * (p.per_row_scales ? r : warp);
-                    store_y(p, T, sr, lane, r0 + r);
+                    if (B == 1 && (p.epi != WW_EPI_NONE || p.pro == WW_PRO_RMSNORM))
+                        store_y_ops(p, T, sr, r0 + r, res, rnorm);
+                    else
+                        store_y(p, T, sr, lane, r0 + r);
                 }
                 if (tr_sweep < 29) trace(tslot, tr_sweep++);
                 acc.zero();
@@ -594,11 +652,35 @@ namespace {
 // one launch of wl_gemv_kernel<B> (arguments already validated)
 ww_status launch_batch(const ww_layer* L, const void* packed_d, const float* scales_d,
                        const float* X_d, int64_t ldx, float* Y_d, int64_t ldy, int32_t B,
-                       void* stream) {
+                       void* stream, const ww_ops* ops = nullptr) {
     ww_launch_info li;
     plan(L, B, num_sms(), &li);
     Params p;
     memset(&p, 0, sizeof p);
+    if (ops) {  // ww_wl_gemv_fused (validated by the caller): B = 1, single tile, TMA
+        p.pro = ops->prologue;
+        p.epi = ops->epilogue;
+        p.eps = ops->eps;
+        p.gamma = ops->gamma;
+        p.residual = ops->residual;
+        p.silu_rows = ops->silu_rows;
+        p.row0 = ops->row0;
+        if (li.path != 0)
+            return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv_fused: x of m=%lld does not fit one tile",
+                            (long long)L->m);
+        if (p.pro == WW_PRO_MUL) {
+            const int64_t T = (ww::words_per_row(L->m) + 31) / 32;
+            const int64_t rows = (L->n + li.grid - 1) / li.grid;
+            const int64_t bytes =
+                smem_layout(1, (int)(32 * T), li.block / 32, true, (int)T, (int)rows, true).total;
+            if (bytes > kSmemBudget)
+                return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv_fused: x and x2 of m=%lld do not fit",
+                                (long long)L->m);
+            li.smem_bytes = (int32_t)bytes;
+            if (ww::encode_x_map(&p.tmap2, ops->x2, ww::words_per_row(L->m), 1, L->m) != 0)
+                return ww::fail(WW_ERR_CUDA, "ww_wl_gemv_fused: tensor map of x2");
+        }
+    }
     p.packed = reinterpret_cast<const uint4*>(packed_d);
     p.scales = scales_d;
     p.X = X_d;
@@ -617,7 +699,9 @@ ww_status launch_batch(const ww_layer* L, const void* packed_d, const float* sca
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
     p.x_stride = (li.tile_chunks + 31) / 32 * 32;
     p.single = li.path == 0;
-    p.use_tma = p.single && !g_force_cp_async ? (encode_x_map(p, B) ? 1 : 0) : 0;
+    p.use_tma = p.single && (ops || !g_force_cp_async) ? (encode_x_map(p, B) ? 1 : 0) : 0;
+    if (ops && !p.use_tma)
+        return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv_fused: needs TMA staging (16 | m, 16-B x)");
     p.dbg = g_debug_flags;
     g_last_use_tma = p.use_tma;
     cudaError_t e = launch(p, li, B, (cudaStream_t)stream, (L->flags & WW_FLAG_PDL) != 0);
@@ -687,4 +771,29 @@ extern "C" ww_status ww_pack_ternary_device(const int8_t* planes_d, int64_t n, i
     if (e != cudaSuccess)
         return ww::fail(WW_ERR_CUDA, "ww_pack_ternary_device: %s", cudaGetErrorString(e));
     return ww::ok();
+}
+
+extern "C" ww_status ww_wl_gemv_fused(const ww_layer* L, const void* packed_d, const float* scales_d,
+                                      const float* x_d, float* y_d, const ww_ops* ops,
+                                      void* stream) {
+    const char* fn = "ww_wl_gemv_fused";
+    ww_status st = check_layer(L, fn);
+    if (st != WW_OK) return st;
+    if (!ops) return ww_wl_gemv(L, packed_d, scales_d, x_d, y_d, stream);
+    if (!packed_d || !scales_d || !x_d || !y_d)
+        return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: null pointer", fn);
+    if (ops->prologue < WW_PRO_NONE || ops->prologue > WW_PRO_MUL || ops->epilogue < WW_EPI_NONE ||
+        ops->epilogue > WW_EPI_SILU || (ops->prologue == WW_PRO_MUL && !ops->x2) ||
+        (ops->prologue == WW_PRO_RMSNORM && (!ops->gamma || !(ops->eps >= 0.f))) ||
+        (ops->epilogue == WW_EPI_RESIDUAL && !ops->residual) || ops->row0 < 0)
+        return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: ops", fn);
+    if (L->m % 16 || ((uintptr_t)x_d & 15) || ((uintptr_t)ops->x2 & 15) ||
+        ((uintptr_t)ops->gamma & 15) || ((uintptr_t)ops->residual & 7) || ((uintptr_t)packed_d & 15) ||
+        ((uintptr_t)y_d & 7) || ((uintptr_t)scales_d & 3))
+        return ww::fail(WW_ERR_MISALIGNED, "%s: needs 16 | m and 16-B aligned x / x2 / gamma", fn);
+    const char* xb = reinterpret_cast<const char*>(x_d);
+    const char* yb = reinterpret_cast<const char*>(y_d);
+    if (xb < yb + 8 * L->n && yb < xb + 8 * L->m)
+        return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: x and y overlap", fn);
+    return launch_batch(L, packed_d, scales_d, x_d, L->m, y_d, L->n, 1, stream, ops);
 }

@@ -87,11 +87,6 @@ __device__ __forceinline__ uint4 lds128u(uint32_t addr) {
                  : "r"(addr));
     return v;
 }
-__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
-    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
-                 "f"(v.w)
-                 : "memory");
-}
 __device__ __forceinline__ void bar_consumers() {  // named barrier 1: the 16 consumer warps
     asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32) : "memory");
 }
@@ -119,7 +114,6 @@ __device__ __forceinline__ float2 ldcg2(const float* p) {  // L2 only: written b
     asm volatile("ld.global.cg.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
     return v;
 }
-__device__ __forceinline__ float silu(float v) { return v / (1.0f + expf(-v)); }
 
 // whole rows of a stage packed into one ring slot (one bulk copy, one full/empty pair)
 __host__ __device__ __forceinline__ int rows_per_slot(int slot_bytes, int row_bytes) {
@@ -231,6 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
                     for (int g = 0; g < p.world; ++g) red_release_sys(p.sync[g], 1u);
             }
         }
+        float4 gam[kGammaRegs];  // RMSNorm gamma (a weight): loaded before the wait
+        float rnorm = 1.0f;
+        if (pro == WW_PRO_RMSNORM) gamma_prefetch(gam, D.gamma, D.m, J, threadIdx.x, kCW * 32);
         if (D.wait && threadIdx.x == 0) {
             const uint32_t target = epoch * (uint32_t)(p.nstages - 1) * T + (uint32_t)s * T;
             if (p.world == 1)
@@ -258,38 +255,14 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
         if (pro != WW_PRO_NONE) {
             const int ng = 8 * 32 * J;
             if (pro == WW_PRO_MUL) {  // x = a (.) b, re and im separately (real view)
-                for (int gi = threadIdx.x; gi < ng; gi += kCW * 32) {
-                    const float4 a = lds128(xa + 16u * gi), b = lds128(xb + 16u * gi);
-                    sts128(xa + 16u * gi, make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w));
-                }
-            } else {  // RMSNorm over the real 2m-vector: x * gamma / sqrt(mean(x^2) + eps)
-                float ss = 0.f;
-                for (int gi = threadIdx.x; gi < ng; gi += kCW * 32) {
-                    const float4 a = lds128(xa + 16u * gi);
-                    ss = ss + a.x * a.x;
-                    ss = ss + a.y * a.y;
-                    ss = ss + a.z * a.z;
-                    ss = ss + a.w * a.w;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                x_mul(xa, xb, ng, threadIdx.x, kCW * 32);
+            } else {  // RMSNorm over the real 2m-vector: x * gamma, 1/rms in the epilogue
+                const float ss =
+                    x_gamma_sumsq_warp(xa, ng, threadIdx.x, kCW * 32, gam, D.gamma, D.m);
                 if (lane == 0) part[warp] = ss;
-                bar_consumers();
-                float tot = 0.f;
-#pragma unroll 1
-                for (int w = 0; w < kCW; ++w) tot += part[w];  // fixed order: deterministic
-                const float r = 1.0f / sqrtf(tot / (float)(2 * D.m) + D.eps);
-                for (int gi = threadIdx.x; gi < ng; gi += kCW * 32) {
-                    const int c = gi >> 3, g = (gi & 7) ^ (c & 7);
-                    const int64_t col = 16 * (int64_t)c + 2 * g;
-                    if (col >= D.m) continue;  // zero padding stays zero
-                    const float4 a = lds128(xa + 16u * gi);
-                    const float4 gm = __ldg(reinterpret_cast<const float4*>(D.gamma + 2 * col));
-                    sts128(xa + 16u * gi, make_float4(a.x * gm.x * r, a.y * gm.y * r,
-                                                      a.z * gm.z * r, a.w * gm.w * r));
-                }
             }
             bar_consumers();
+            if (pro == WW_PRO_RMSNORM) rnorm = rms_factor(part, kCW, D.m, D.eps);
         }
 
         // ---- the warp's rows, in units of up to rps consecutive rows per ring slot:
@@ -352,12 +325,16 @@ __global__ void __launch_bounds__(kThreads, 1) wl_program_kernel(const __grid_co
                 float yim = conv == WW_CONV_EQ1
                                 ? sc.x * Tt[1] + sc.y * Tt[2] - sc.z * Tt[5] + sc.w * Tt[6]   // Eq. 1
                                 : sc.x * Tt[1] + sc.y * Tt[2] + sc.z * Tt[5] - sc.w * Tt[6];  // Eq. 3
+                if (pro == WW_PRO_RMSNORM) {  // RMSNorm scalar (linear map)
+                    yre = yre * rnorm;
+                    yim = yim * rnorm;
+                }
                 if (epi == WW_EPI_RESIDUAL) {
                     yre = yre + res.x;
                     yim = yim + res.y;
                 } else if (epi == WW_EPI_SILU && grow < silu_rows) {
-                    yre = silu(yre);
-                    yim = silu(yim);
+                    yre = silu_f(yre);
+                    yim = silu_f(yim);
                 }
                 ydst0[grow] = make_float2(yre, yim);
                 for (int g = 1; g < ndst; ++g)

@@ -331,4 +331,106 @@ __device__ __forceinline__ void reduce_to(const Acc<B>& acc, float* dst) {
     __syncwarp();
 }
 
+
+// ---------------------------------------------------------------- fused decode-block ops
+// (NEXT-3) on a staged, 128B-swizzled x region of 8*32*J 16-byte granules (2
+// complex columns each), shared by the per-stage kernel and the program kernel so both give
+// the same bits.  Granule gi of chunk c = gi >> 3 sits at physical slot gi & 7 and holds
+// logical granule (gi & 7) ^ (c & 7), i.e. columns 16c + 2g, +1.
+
+__device__ __forceinline__ void sts128_f4(uint32_t addr, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+
+// x <- x (.) x2 on the real view (re*re, im*im): SiLU(gate) (.) up
+__device__ __forceinline__ void x_mul(uint32_t xa, uint32_t xb, int ng, int tid, int nthr) {
+    for (int gi = tid; gi < ng; gi += nthr) {
+        const float4 a = lds128(xa + 16u * gi), b = lds128(xb + 16u * gi);
+        sts128_f4(xa + 16u * gi, make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w));
+    }
+}
+
+// RMSNorm in one pass: x <- x * gamma in place while summing x^2 over the real
+// 2m-vector; the scalar 1 / sqrt(mean(x^2) + eps) is applied to the row results in the
+// epilogue (the map is linear: WL(r v) = r WL(v)).  g[k] = this thread's gamma granules,
+// loaded before the readiness wait (gamma is a weight); returns the warp-reduced partial sum
+// (xor butterfly, the same order for every caller).
+constexpr int kGammaRegs = 4;  // gamma granules a thread holds in registers (J <= 8 at 512 thr.)
+__device__ __forceinline__ void gamma_prefetch(float4 (&g)[kGammaRegs], const float* gamma,
+                                               int64_t m, int J, int tid, int nthr) {
+#pragma unroll
+    for (int k = 0; k < kGammaRegs; ++k) {
+        const int gi = tid + k * nthr;
+        const int c = gi >> 3, gg = (gi & 7) ^ (c & 7);
+        const int64_t col = 16 * (int64_t)c + 2 * gg;
+        g[k] = (gi < 8 * 32 * J && col < m) ? __ldg(reinterpret_cast<const float4*>(gamma + 2 * col))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+__device__ __forceinline__ float x_gamma_sumsq_warp(uint32_t xa, int ng, int tid, int nthr,
+                                                    const float4 (&g)[kGammaRegs],
+                                                    const float* gamma, int64_t m) {
+    float ss = 0.f;
+    auto one = [&](int gi, float4 gm) {
+        const float4 a = lds128(xa + 16u * gi);
+        ss = ss + a.x * a.x;
+        ss = ss + a.y * a.y;
+        ss = ss + a.z * a.z;
+        ss = ss + a.w * a.w;
+        sts128_f4(xa + 16u * gi, make_float4(a.x * gm.x, a.y * gm.y, a.z * gm.z, a.w * gm.w));
+    };
+#pragma unroll
+    for (int k = 0; k < kGammaRegs; ++k)
+        if (tid + k * nthr < ng) one(tid + k * nthr, g[k]);
+    for (int gi = tid + kGammaRegs * nthr; gi < ng; gi += nthr) {  // wide x: load gamma here
+        const int c = gi >> 3, gg = (gi & 7) ^ (c & 7);
+        const int64_t col = 16 * (int64_t)c + 2 * gg;
+        one(gi, col < m ? __ldg(reinterpret_cast<const float4*>(gamma + 2 * col))
+                        : make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    return ss;
+}
+
+// this thread's share of sum(x^2) over the real 2m-vector, then reduced over the warp
+// (xor butterfly, the same order for every caller)
+__device__ __forceinline__ float x_sumsq_warp(uint32_t xa, int ng, int tid, int nthr) {
+    float ss = 0.f;
+    for (int gi = tid; gi < ng; gi += nthr) {
+        const float4 a = lds128(xa + 16u * gi);
+        ss = ss + a.x * a.x;
+        ss = ss + a.y * a.y;
+        ss = ss + a.z * a.z;
+        ss = ss + a.w * a.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    return ss;
+}
+
+// RMSNorm factor from the per-warp partial sums (fixed order: deterministic)
+__device__ __forceinline__ float rms_factor(const float* part, int nwarps, int64_t m, float eps) {
+    float tot = 0.f;
+    for (int w = 0; w < nwarps; ++w) tot += part[w];
+    return 1.0f / sqrtf(tot / (float)(2 * m) + eps);
+}
+
+// x <- (x * gamma) * r (gamma: 2m fp32 over the real view)
+__device__ __forceinline__ void x_rms_scale(uint32_t xa, int ng, int tid, int nthr,
+                                            const float* gamma, int64_t m, float r) {
+    for (int gi = tid; gi < ng; gi += nthr) {
+        const int c = gi >> 3, g = (gi & 7) ^ (c & 7);
+        const int64_t col = 16 * (int64_t)c + 2 * g;
+        if (col >= m) continue;  // zero padding stays zero
+        const float4 a = lds128(xa + 16u * gi);
+        const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma + 2 * col));
+        sts128_f4(xa + 16u * gi, make_float4(a.x * gm.x * r, a.y * gm.y * r, a.z * gm.z * r,
+                                            a.w * gm.w * r));
+    }
+}
+
+__device__ __forceinline__ float silu_f(float v) { return v / (1.0f + expf(-v)); }
 }  // namespace

@@ -85,9 +85,14 @@ class WLStack:
 
     def __init__(self, layers: int = wi.C4_LAYERS, seed: int = 0, B: int = 1, rank: int = 0,
                  world: int = 1, conv: int = CONV_EQ1, pdl: bool = True, device=None,
-                 group=None, fuse: bool = True):
+                 group=None, fuse: bool = True, chain: str = "plain", gammas=None):
+        """chain "plain": every stage reads its own seeded x; "block": the NEXT-3 decode-block
+        chain (block_inputs), stage inputs are earlier stages' gathered outputs, with the
+        fused RMSNorm / SiLU / (.) / residual ops of ww_wl_gemv_fused (B = 1, fuse = True)."""
         self.layers, self.seed, self.B, self.rank, self.world = layers, seed, B, rank, world
-        self.conv, self.group = conv, group
+        self.conv, self.group, self.chain, self.gammas = conv, group, chain, gammas
+        if chain == "block":
+            assert B == 1 and fuse and gammas is not None
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.flags = FLAG_PDL if pdl else 0
         self.stages: list[Stage] = []
@@ -143,6 +148,10 @@ class WLStack:
         self.X.copy_(torch.from_numpy(xs_host))
         torch.cuda.synchronize(self.device)
 
+    def inputs(self):
+        """The step's host-fed inputs: every stage's x (plain), or h_0 alone (block chain)."""
+        return self.X if self.chain == "plain" else self.X[:self.stages[0].m]
+
     def x_of(self, st: Stage):
         return self.X[st.xoff:st.xoff + self.B * st.m].view(self.B, st.m)
 
@@ -167,6 +176,15 @@ class WLStack:
         if not st.ylocal:
             return 0
         L = Layer(st.ylocal, st.m, LAYOUT_COL4, SCALES_PER_ROW, self.conv, self.flags)
+        if self.chain == "block":
+            from . import Ops, wl_gemv_fused
+            kw = block_inputs(self, i, self.gammas)
+            x = kw.pop("x")
+            wl_gemv_fused(L, self.W[st.off:st.off + st.nbytes],
+                          self.S[st.soff:st.soff + 4 * st.ylocal], x,
+                          self.y_local_view(st)[0], Ops(row0=st.shard.row_begin, **kw),
+                          stream=stream)
+            return 1
         wl_gemv_batched(L, self.W[st.off:st.off + st.nbytes],
                         self.S[st.soff:st.soff + 4 * st.ylocal], self.x_of(st),
                         self.y_local_view(st), stream=stream)
@@ -224,6 +242,33 @@ def block_gammas(seed: int, layers: int, m: int):
     return out
 
 
+def block_inputs(part: "WLStack", i: int, gammas, x0=None) -> dict:
+    """Input and fused ops of stage i in the NEXT-3 decode-block chain, on this
+    rank's copies of the gathered outputs (part.Y): per layer l
+      qkv   x = RMSNorm(h_l; gamma_attn)            -> QKV_l
+      o     x = v = QKV_l[4096:6144], + residual h_l -> H1_l   (attention = identity on v)
+      gateup x = RMSNorm(H1_l; gamma_mlp), SiLU on the gate rows -> GU_l
+      down  x = SiLU(gate) (.) up = GU_l[:5504] (.) GU_l[5504:], + residual H1_l -> h_{l+1}
+    with h_0 = x0 (default: stage 0's seeded x).  Returns x and the ww_ops fields."""
+    from . import EPI_RESIDUAL, EPI_SILU, PRO_MUL, PRO_RMSNORM
+    st = part.stages[i]
+    Yl = part.Y
+    l = st.layer
+    base = 4 * l
+    h_l = (x0 if x0 is not None else part.x_of(part.stages[0])[0]) if l == 0 else Yl[base - 1]
+    if st.name == "qkv":
+        return dict(x=h_l, prologue=PRO_RMSNORM, gamma=gammas[l][0], eps=EPS)
+    if st.name == "o":
+        return dict(x=Yl[base][4096:6144], epilogue=EPI_RESIDUAL, residual=h_l)
+    if st.name == "gateup":
+        return dict(x=Yl[base + 1], prologue=PRO_RMSNORM, gamma=gammas[l][1], eps=EPS,
+                    epilogue=EPI_SILU, silu_rows=5504)
+    if st.name == "down":
+        return dict(x=Yl[base + 2][:5504], x2=Yl[base + 2][5504:11008], prologue=PRO_MUL,
+                    epilogue=EPI_RESIDUAL, residual=Yl[base + 1])
+    raise ValueError(st.name)
+
+
 def program_stages(part: "WLStack", parts: list, mode: str = "plain", gammas=None,
                    x0=None):
     """ww_stage list of one rank (`part`) for a persistent program over its WLStack; the
@@ -235,8 +280,7 @@ def program_stages(part: "WLStack", parts: list, mode: str = "plain", gammas=Non
       gateup x = RMSNorm(H1_l; gamma_mlp), SiLU on the gate rows -> GU_l
       down  x = SiLU(gate) (.) up = GU_l[:5504] (.) GU_l[5504:], + residual H1_l -> h_{l+1}
     with h_0 = x0 (default: stage 0's seeded x).  gammas: block_gammas() as device tensors."""
-    from . import (EPI_NONE, EPI_RESIDUAL, EPI_SILU, PRO_MUL, PRO_NONE, PRO_RMSNORM,
-                   SCALES_PER_ROW, Stage)
+    from . import SCALES_PER_ROW, Stage
     world = part.world
     assert part.B == 1 and len(parts) == world
     st_list = []
@@ -249,22 +293,7 @@ def program_stages(part: "WLStack", parts: list, mode: str = "plain", gammas=Non
         if mode == "plain":
             kw.update(x=part.x_of(st)[0])
         elif mode == "block":
-            Yl = part.Y  # this rank's copies of the gathered outputs
-            l = st.layer
-            base = 4 * l
-            h_l = (x0 if x0 is not None else part.x_of(part.stages[0])[0]) if l == 0 else Yl[base - 1]
-            if st.name == "qkv":
-                kw.update(x=h_l, prologue=PRO_RMSNORM, gamma=gammas[l][0], eps=EPS)
-            elif st.name == "o":
-                kw.update(x=Yl[base][4096:6144], epilogue=EPI_RESIDUAL, residual=h_l)
-            elif st.name == "gateup":
-                kw.update(x=Yl[base + 1], prologue=PRO_RMSNORM, gamma=gammas[l][1], eps=EPS,
-                          epilogue=EPI_SILU, silu_rows=5504)
-            elif st.name == "down":
-                kw.update(x=Yl[base + 2][:5504], x2=Yl[base + 2][5504:11008], prologue=PRO_MUL,
-                          epilogue=EPI_RESIDUAL, residual=Yl[base + 1])
-            else:
-                raise ValueError(st.name)
+            kw.update(block_inputs(part, i, gammas, x0))
         else:
             raise ValueError(mode)
         st_list.append(Stage(**kw))

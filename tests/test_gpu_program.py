@@ -169,3 +169,48 @@ def test_decode_block_matches_oracle_stage_by_stage(world):
         h, _ = orc.block_forward(layer, h, gam_h[l])
     rel = np.linalg.norm(Y[-1] - h) / np.linalg.norm(h)
     assert rel <= 1e-5, rel
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_per_stage_kernel_block_chain_bitwise_equals_program(world):
+    # the same fused ops in the per-stage PDL kernel (ww_wl_gemv_fused) and in the program
+    # kernel share their device code: the decode-block chain agrees bit for bit; at world 2
+    # the per-stage ranks exchange by copies (NCCL is the product exchange, tested on >= 2 GPUs)
+    layers = 2
+    gam = [tuple(torch.from_numpy(g).cuda() for g in pair) for pair in block_gammas(3, layers, 2048)]
+    ref = WLStack(layers=layers, seed=3)
+    ww.Program([program_stages(ref, [ref], "block", gam)]).run()
+    parts = [WLStack(layers=layers, seed=3, rank=r, world=world, chain="block", gammas=gam)
+             for r in range(world)]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for i in range(len(parts[0].stages)):
+            for p in parts:
+                p.launch(i, s)
+            for p in parts:  # emulated all-gather of stage i
+                n = p.Y[i].numel() // world
+                for q in parts:
+                    if q is not p:
+                        q.Y[i][p.rank * n:(p.rank + 1) * n].copy_(p.Y[i][p.rank * n:(p.rank + 1) * n])
+    torch.cuda.synchronize()
+    for i, st in enumerate(ref.stages):
+        for p in parts:
+            assert torch.equal(p.gathered(p.stages[i]), ref.gathered(st)), (st.label, p.rank)
+
+
+def test_fused_ops_argument_errors():
+    case_n, m = 64, 2048
+    packed = torch.zeros(ww.packed_bytes(case_n, m), dtype=torch.uint8, device="cuda")
+    sc = torch.ones((case_n, 4), device="cuda")
+    x = torch.zeros(m, dtype=torch.complex64, device="cuda")
+    L = ww.Layer(case_n, m)
+    with pytest.raises(ww.WWError) as e:  # MUL without its second operand
+        ww.wl_gemv_fused(L, packed, sc, x, ops=ww.Ops(prologue=ww.PRO_MUL))
+    assert e.value.status == ww.ERR_INVALID_ARGUMENT
+    with pytest.raises(ww.WWError) as e:  # 16 does not divide m: no TMA staging
+        L2 = ww.Layer(case_n, 100)
+        ww.wl_gemv_fused(L2, packed, sc, x[:100], ops=ww.Ops(epilogue=ww.EPI_SILU, silu_rows=10))
+    assert e.value.status == ww.ERR_MISALIGNED
+    y = ww.wl_gemv_fused(L, packed, sc, x, ops=None)  # no ops == ww_wl_gemv
+    torch.cuda.synchronize()
+    assert not torch.view_as_real(y).any()
