@@ -274,7 +274,8 @@ def run_ours(args, world, rank, local):
                    for pair in block_gammas(args.seed, args.layers, 2048)]
         base = WLStack(layers=args.layers, seed=args.seed, B=args.batch, rank=rank, world=world,
                        pdl=not args.no_pdl, device=dev, group=group, fuse=not args.no_fuse,
-                       chain=args.chain if args.engine == "pdl" else "plain", gammas=gam)
+                       chain=args.chain if args.engine == "pdl" else "plain", gammas=gam,
+                       symm=args.engine == "program" and world > 1)
         if args.engine == "program":
             stack = ProgramRunner(base, args.chain, gam)
         else:
@@ -566,11 +567,12 @@ class ProgramRunner:
     def __init__(self, base, chain, gam):
         import paper_2604_20913_b200 as ww
         from paper_2604_20913_b200.stack import program_stages
-        if base.world != 1:
-            raise SystemExit("--engine program at world > 1 needs peer-mapped outputs (not wired "
-                             "in bench.py); use the default engine")
         self.base, self.chain, self.gam = base, chain, gam
-        self.prog = ww.Program([program_stages(base, [base], chain, gam)], world=1)
+        if base.world == 1:
+            self.prog = ww.Program([program_stages(base, [base], chain, gam)], world=1)
+        else:  # one rank per GPU: outputs and sync words in symmetric memory (NEXT-1)
+            self.prog = ww.Program([program_stages(base, None, chain, gam)], world=base.world,
+                                   rank_base=base.rank, sync=base.symm.sync_ptrs())
         self.stages, self.X, self.Y = base.stages, base.X, base.Y
 
     def step(self, stream=None):

@@ -352,6 +352,12 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
 #endif
                 pdl_wait();
             trace(tslot, 2);
+            if (p.use_tma) {
+                stage_x_regions_tma<B>(p, xs, bars);
+            } else {
+                stage_x_regions_cp_async<B>(p, xs, bars);
+            }
+            // (x first: the scales are needed only at the end of the warp's first row)
             // the warp's row scales -> shared memory (cp.async), after griddepcontrol.wait so
             // a preceding kernel may write them (ww.h WW_FLAG_PDL); per-row mode: rows
             // [w0, w1) at slot r, per-tensor mode: the 4 scales at the warp's own slot.  The
@@ -366,11 +372,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                     cp_async4(sdst + 16u * warp + 4u * lane, p.scales + lane);
                 }
             }
-            if (p.use_tma) {
-                stage_x_regions_tma<B>(p, xs, bars);
-            } else {
-                stage_x_regions_cp_async<B>(p, xs, bars);
-            }
+
             trace(tslot, 3);
             int tr_sweep = 4;
 

@@ -80,12 +80,59 @@ class Stage:
         return f"L{self.layer}.{self.name}"
 
 
+SYNC_BYTES = 2048  # ww_program_sync_bytes()
+
+
+def peer_address(local_ptr: int, local_base: int, peer_base: int) -> int:
+    """The same byte of a symmetric buffer as mapped from another rank: buffers are laid out
+    identically on every rank, so an offset from the local base is an offset from any peer's
+    base."""
+    assert local_ptr >= local_base
+    return peer_base + (local_ptr - local_base)
+
+
+def symm_layout(counts, align: int = 256):
+    """Byte offsets of the per-stage gathered outputs (complex64 counts) and of the sync words
+    inside one symmetric buffer; returns (offsets, sync_offset, total_bytes)."""
+    offs, o = [], 0
+    for c in counts:
+        offs.append(o)
+        o += (8 * c + align - 1) // align * align
+    return offs, o, o + SYNC_BYTES
+
+
+class SymmOutputs:
+    """One symmetric-memory buffer per rank holding every stage's gathered output and the
+    program's sync words; `bases[g]` = rank g's mapping of it (peer pointers, NVLink)."""
+
+    def __init__(self, counts, device, group):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        offs, sync_off, total = symm_layout(counts)
+        self.buf = symm_mem.empty(total, dtype=torch.uint8, device=device)
+        self.buf.zero_()
+        torch.cuda.synchronize(device)
+        self.handle = symm_mem.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
+        self.bases = [int(p) for p in self.handle.buffer_ptrs]
+        self.local = self.buf.data_ptr()
+        self.views = [self.buf[o:o + 8 * c].view(torch.complex64) for o, c in zip(offs, counts)]
+        self.sync_off = sync_off
+        dist.barrier(group=group)
+
+    def peer(self, t, g: int) -> int:
+        return peer_address(t.data_ptr(), self.local, self.bases[g])
+
+    def sync_ptrs(self):
+        return [b + self.sync_off for b in self.bases]
+
+
 class WLStack:
     """All stages of the stack resident in HBM on one rank (its row shard of every stage)."""
 
     def __init__(self, layers: int = wi.C4_LAYERS, seed: int = 0, B: int = 1, rank: int = 0,
                  world: int = 1, conv: int = CONV_EQ1, pdl: bool = True, device=None,
-                 group=None, fuse: bool = True, chain: str = "plain", gammas=None):
+                 group=None, fuse: bool = True, chain: str = "plain", gammas=None,
+                 symm: bool = False):
         """chain "plain": every stage reads its own seeded x; "block": the NEXT-3 decode-block
         chain (block_inputs), stage inputs are earlier stages' gathered outputs, with the
         fused RMSNorm / SiLU / (.) / residual ops of ww_wl_gemv_fused (B = 1, fuse = True)."""
@@ -118,9 +165,17 @@ class WLStack:
         self.W = torch.empty(max(off, 16), dtype=torch.uint8, device=self.device)
         self.S = torch.empty(max(soff, 4), dtype=torch.float32, device=self.device)
         self.X = torch.empty(max(xoff, 1), dtype=torch.complex64, device=self.device)
-        # gathered outputs: [world][B][rows_per_rank] per stage (rank-major, ww.h)
-        self.Y = [torch.zeros(st.shard.n_padded * B, dtype=torch.complex64, device=self.device)
-                  for st in self.stages]
+        # gathered outputs: [world][B][rows_per_rank] per stage (rank-major, ww.h); with
+        # symm=True they (and the program's readiness words) live in ONE symmetric-memory
+        # buffer every rank maps (torch.distributed._symmetric_memory), so the program kernel
+        # can store rows straight into every peer's copy (fused all-gather, NEXT-1)
+        counts = [st.shard.n_padded * B for st in self.stages]
+        self.symm = None
+        if symm:
+            self.symm = SymmOutputs(counts, self.device, group)
+            self.Y = self.symm.views
+        else:
+            self.Y = [torch.zeros(c, dtype=torch.complex64, device=self.device) for c in counts]
         self._fill()
 
     # ------------------------------------------------------------------ inputs
@@ -282,10 +337,14 @@ def program_stages(part: "WLStack", parts: list, mode: str = "plain", gammas=Non
     with h_0 = x0 (default: stage 0's seeded x).  gammas: block_gammas() as device tensors."""
     from . import SCALES_PER_ROW, Stage
     world = part.world
-    assert part.B == 1 and len(parts) == world
+    assert part.B == 1
     st_list = []
     for i, st in enumerate(part.stages):
-        ys = [parts[g].Y[i] for g in range(world)]
+        if parts is None:  # one rank per process: peer-mapped symmetric outputs
+            ys = [part.symm.peer(part.Y[i], g) for g in range(world)]
+        else:  # every rank's buffers in this process (one-GPU emulation)
+            assert len(parts) == world
+            ys = [parts[g].Y[i] for g in range(world)]
         kw = dict(packed=part.W[st.off:st.off + max(st.nbytes, 16)],
                   scales=part.S[st.soff:st.soff + max(4 * st.ylocal, 4)],
                   n_local=st.ylocal, row0=st.shard.row_begin, m=st.m, y=ys,
