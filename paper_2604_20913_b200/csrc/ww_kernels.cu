@@ -29,6 +29,9 @@
 #include "ww_internal.h"
 #include "ww_sweep.cuh"
 
+#ifndef WW_SWEEP_UNROLL2
+#define WW_SWEEP_UNROLL2 0  // experiment switch (tools/build.py --variant)
+#endif
 #ifndef WW_DEBUG_FLAGS
 #define WW_DEBUG_FLAGS 0  // 1: honour Params::dbg (tools/chain_time.py builds build/libww_dbg.so)
 #endif
@@ -402,6 +405,29 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 float2 res = make_float2(0.f, 0.f);  // WW_EPI_RESIDUAL operand, a row ahead
                 if (B == 1 && p.epi == WW_EPI_RESIDUAL && lane == 0)
                     res = __ldcg(reinterpret_cast<const float2*>(p.residual) + p.row0 + r0 + r);
+#if WW_SWEEP_UNROLL2
+                // two sweeps per iteration: the second sweep's x sits 4096 B above the
+                // first's with the same swizzle key, so its LDS use immediate offsets
+#pragma unroll 1
+                for (int k = 0; k + 1 < J; k += 2) {
+                    uint4 cur = qa;
+                    qa = qb;
+                    qb = load_next();
+                    chunk<B>(acc, cur, xc, bstride, 0u);
+                    cur = qa;
+                    qa = qb;
+                    qb = load_next();
+                    chunk<B>(acc, cur, xc, bstride, 4096u);
+                    xc += 8192u;
+                }
+                if (J & 1) {
+                    const uint4 cur = qa;
+                    qa = qb;
+                    qb = load_next();
+                    chunk<B>(acc, cur, xc, bstride);
+                    xc += 4096u;
+                }
+#else
 #pragma unroll 1
                 for (int k = 0; k < J; ++k) {
                     const uint4 cur = qa;
@@ -414,6 +440,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                         chunk<B>(acc, cur, xc, bstride);
                     xc += 4096u;
                 }
+#endif
                 // reduce the row over the lanes (a7) into the CTA's totals
                 reduce_to<B>(acc, tot + r * NV);
                 if (r == w0) {  // before the warp's first epilogue: its scale copies have landed
@@ -524,7 +551,10 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     const int64_t W = ww::words_per_row(L->m);
     const int warps = warps_for_b(B);
     // one CTA per SM (persistent), each owning a contiguous, balanced row range
-    const int64_t grid = std::min<int64_t>(sms, L->n);
+#ifndef WW_CTAS_PER_SM
+#define WW_CTAS_PER_SM 1  // experiment switch: B = 1 launches with 2 CTAs per SM (tools only)
+#endif
+    const int64_t grid = std::min<int64_t>((B == 1 ? WW_CTAS_PER_SM : 1) * (int64_t)sms, L->n);
     const int64_t rows = (L->n + grid - 1) / grid;  // rows per CTA (at most)
     // Single x tile: the whole row is one work unit of T = ceil(W/32) sweeps (x must fit
     // kXBudgetBytes); else column tiles.  (Splitting rows into column parts handed between

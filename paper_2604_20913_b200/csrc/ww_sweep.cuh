@@ -117,8 +117,11 @@ __device__ __forceinline__ void mbar_wait0(uint32_t bar) { mbar_wait(bar, 0); }
 // 5-10 % slower: register pressure.)
 template <int B>
 struct Acc {
-    static constexpr int S = B <= 2 ? 2 : 1;  // column-parity sets
-    static constexpr int N = 1;
+#ifndef WW_ACC_POSNEG
+#define WW_ACC_POSNEG 0  // experiment switch: B = 1 keeps +1 and -1 sums apart (S = 1, N = 2)
+#endif
+    static constexpr int S = (B == 1 && WW_ACC_POSNEG) ? 1 : (B <= 2 ? 2 : 1);  // column-parity sets
+    static constexpr int N = (B == 1 && WW_ACC_POSNEG) ? 2 : 1;
     float2 a[S][N][B][4];
     __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -205,7 +208,10 @@ __device__ __forceinline__ void column(float2 (&pos)[4], float2 (&neg)[4], uint3
 // vector b at + b*bstride): granule kk (columns 2kk, 2kk+1) sits at xl ^ (kk << 4), one LOP3
 // per load (the 128B swizzle of the TMA boxes; 32 lanes on 32 chunks hit 32 banks).
 template <int B>
-__device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xl, uint32_t bstride) {
+__device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xl, uint32_t bstride,
+                                      uint32_t off = 0) {
+    // off: a multiple of 4096 added after the swizzle (the chunk 32 sweeps later sits at the
+    // same swizzle key), so two sweeps can share the swizzled addresses with immediate offsets
     constexpr int S = Acc<B>::S, N = Acc<B>::N;
     const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -213,7 +219,7 @@ __device__ __forceinline__ void chunk(Acc<B>& acc, const uint4 w, uint32_t xl, u
         const uint32_t word = w4[kk >> 1];
         const uint32_t sh = (kk & 1) * 16;
         const uint32_t bits_a = (word >> sh) & 0xffu, bits_b = (word >> (sh + 8)) & 0xffu;
-        const uint32_t xa = xl ^ ((uint32_t)kk << 4);
+        const uint32_t xa = (xl ^ ((uint32_t)kk << 4)) + off;
 #if WW_ABL_NO_O2
         if (B == 1) {  // every plane re-loads x: 4 loads per column instead of one per pair
 #pragma unroll

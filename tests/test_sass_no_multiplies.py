@@ -73,3 +73,20 @@ def _check_epilogue(sass):
         before = [j for j in fadd2 if j < i]
         after = [j for j in fadd2 if j > i]
         assert not (before and after and after[0] - before[-1] <= 8), sass[i]
+
+
+def test_program_kernel_accumulation_loop_has_no_fp_multiply():
+    # the persistent program kernel (ww_program_*) runs the same sweep from shared memory
+    for k in _kernels_sass(r"_ZN\S*wl_program_kernel"):
+        _check_loop(1, [_strip(l) for l in k])
+        _check_epilogue([_strip(l) for l in k])
+
+
+def test_fused_ops_multiplies_stay_outside_the_loop():
+    # the decode-block prologue (RMSNorm, product) and the epilogue (1/rms, SiLU) multiply;
+    # the accumulation blocks of every B = 1 kernel still do not
+    for pat in (r"_ZN\S*wl_gemv_kernelILi1E", r"_ZN\S*wl_program_kernel"):
+        for k in _kernels_sass(pat):
+            s = [_strip(l) for l in k]
+            assert sum(1 for l in s if re.search(r"\bFMUL\b", l)) > 8  # ops present
+            _check_loop(1, s)
