@@ -29,6 +29,9 @@
 #include "ww_internal.h"
 #include "ww_sweep.cuh"
 
+#ifndef WW_X_LDG
+#define WW_X_LDG 0  // experiment switch: x staged by plain 16-B loads of every thread
+#endif
 #ifndef WW_SWEEP_UNROLL2
 #define WW_SWEEP_UNROLL2 0  // experiment switch (tools/build.py --variant)
 #endif
@@ -355,7 +358,18 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
 #endif
                 pdl_wait();
             trace(tslot, 2);
-            if (p.use_tma) {
+            if (WW_X_LDG && B == 1 && p.use_tma && p.pro == WW_PRO_NONE) {
+                // experiment: every thread loads its x granules (16 B) and stores them swizzled
+                const int ng = 8 * 32 * J;
+                const float4* xg = reinterpret_cast<const float4*>(p.X);
+                for (int gi = threadIdx.x; gi < ng; gi += blockDim.x) {
+                    const int c = gi >> 3, g = gi & 7;
+                    const int64_t col = 16 * (int64_t)c + 2 * g;
+                    const float4 v = col < p.m ? __ldcg(xg + (col >> 1)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    sts128_f4(xs + 16u * (uint32_t)(c * 8 + (g ^ (c & 7))), v);
+                }
+                __syncthreads();
+            } else if (p.use_tma) {
                 stage_x_regions_tma<B>(p, xs, bars);
             } else {
                 stage_x_regions_cp_async<B>(p, xs, bars);
@@ -396,8 +410,8 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 }
                 __syncthreads();
                 if (p.pro == WW_PRO_RMSNORM) rnorm = rms_factor(part, nwarps, p.m, p.eps);
-            } else if (w0 < w1) {  // x slices in before the warp's first sweep
-                for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * j);
+            } else if (w0 < w1 && !(WW_X_LDG && B == 1 && p.use_tma)) {  // x slices in before
+                for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * j);     // the warp's first sweep
             }
 #pragma unroll 1
             for (int r = w0; r < w1; ++r) {

@@ -120,7 +120,10 @@ struct Acc {
 #ifndef WW_ACC_POSNEG
 #define WW_ACC_POSNEG 0  // experiment switch: B = 1 keeps +1 and -1 sums apart (S = 1, N = 2)
 #endif
-    static constexpr int S = (B == 1 && WW_ACC_POSNEG) ? 1 : (B <= 2 ? 2 : 1);  // column-parity sets
+#ifndef WW_ACC_S_B4
+#define WW_ACC_S_B4 1  // experiment switch: column-parity sets at 3 <= B <= 4
+#endif
+    static constexpr int S = (B == 1 && WW_ACC_POSNEG) ? 1 : (B <= 2 ? 2 : (B <= 4 ? WW_ACC_S_B4 : 1));
     static constexpr int N = (B == 1 && WW_ACC_POSNEG) ? 2 : 1;
     float2 a[S][N][B][4];
     __device__ __forceinline__ void zero() {
