@@ -203,9 +203,14 @@ def test_device_packer_bit_exact():
     want = ww.pack_ternary(planes, ww.LAYOUT_COL4).view(np.uint8)
     assert np.array_equal(got.cpu().numpy(), want) and int(bad.item()) == 0
     d[2, 5, 7] = 3
-    ww.pack_ternary_device(d, bad)
+    got = ww.pack_ternary_device(d, bad)
     torch.cuda.synchronize()
     assert int(bad.item()) == 1
+    # only the bad column packs as zero: its word-mates 4..6 keep their codes
+    fixed = planes.copy()
+    fixed[:, 5, 7] = 0
+    want = ww.pack_ternary(fixed, ww.LAYOUT_COL4).view(np.uint8)
+    assert np.array_equal(got.cpu().numpy(), want)
 
 
 def test_device_generated_codes_pack_like_host():
