@@ -344,8 +344,10 @@ def test_pdl_chain_reads_previous_layers_output(B, graph):
         ww.wl_gemv_batched(L3, c3.packed_d, sc3, c3.x_d, Y3, stream=s)
 
     def bufs():
-        return [torch.full((B, n), float("nan"), dtype=torch.complex64, device="cuda")
-                for n in (n1, n2, n2)]
+        out = [torch.empty((B, n), dtype=torch.complex64, device="cuda") for n in (n1, n2, n2)]
+        for t in out:
+            torch.view_as_real(t).fill_(float("nan"))  # both parts (a complex fill gives nan+0j)
+        return out
 
     ref = bufs()
     torch.cuda.synchronize()
@@ -365,7 +367,7 @@ def test_pdl_chain_reads_previous_layers_output(B, graph):
     for _ in range(5):
         with torch.cuda.stream(s):
             for t in got:
-                t.fill_(float("nan"))
+                torch.view_as_real(t).fill_(float("nan"))
             if graph:
                 g.replay()
             else:

@@ -214,3 +214,52 @@ def test_fused_ops_argument_errors():
     y = ww.wl_gemv_fused(L, packed, sc, x, ops=None)  # no ops == ww_wl_gemv
     torch.cuda.synchronize()
     assert not torch.view_as_real(y).any()
+
+
+def test_program_per_tensor_scales_alg1_and_empty_shards():
+    # per-tensor scales, ALG1, and a 3-row stage over 4 emulated ranks (rank 3 owns no rows)
+    n, m, world = 3, 512, 4
+    planes = wi.planes(41, n, m, wi.UNIFORM3)
+    scales = wi.scales(41, n, False, 0.5, 2.0)
+    x = wi.activations(41, m)
+    packed = torch.from_numpy(ww.pack_ternary(planes).view(np.uint8)).cuda()
+    sc = torch.from_numpy(scales).cuda()
+    xd = torch.from_numpy(x[0]).cuda()
+    ys = [torch.empty((4 * world,), dtype=torch.complex64, device="cuda") for _ in range(world)]
+    for y in ys:
+        torch.view_as_real(y).fill_(float("nan"))  # (torch.full with a complex nan: nan + 0j)
+    stages = []
+    for r in range(world):
+        sh = ww.shard_plan(n, m, world, r)
+        nl = sh.row_end - sh.row_begin
+        pk = packed[sh.packed_offset_bytes:sh.packed_offset_bytes + max(sh.packed_bytes, 16)]
+        stages.append([ww.Stage(packed=pk, scales=sc, n_local=nl, row0=sh.row_begin, m=m, x=xd,
+                                y=ys, scale_mode=ww.SCALES_PER_TENSOR, conv=ww.CONV_ALG1, wait=0)])
+    ww.Program(stages, world=world).run()
+    torch.cuda.synchronize()
+    ref = orc.wl_direct(orc.pack_planar(planes), n, m, scales, x, orc.CONV_ALG1)
+    for g in range(world):
+        got = ys[g][:n].cpu().numpy()[None]
+        ok, rel, worst = orc.tolerance_check(got, ref, scales, x)
+        assert ok, (g, rel, worst)
+        assert torch.isnan(torch.view_as_real(ys[g][n:])).all()  # nothing written past n
+
+
+def test_program_init_argument_errors():
+    x = torch.zeros(2048, dtype=torch.complex64, device="cuda")
+    y = torch.zeros(16, dtype=torch.complex64, device="cuda")
+    pk = torch.zeros(ww.packed_bytes(16, 2048), dtype=torch.uint8, device="cuda")
+    sc = torch.ones((16, 4), device="cuda")
+    bad_m = ww.Stage(packed=pk, scales=sc, n_local=16, row0=0, m=100, x=x, y=[y], wait=0)
+    with pytest.raises(ww.WWError) as e:
+        ww.Program([[bad_m]])
+    assert e.value.status == ww.ERR_INVALID_ARGUMENT
+    mul_no_x2 = ww.Stage(packed=pk, scales=sc, n_local=16, row0=0, m=2048, x=x, y=[y], wait=0,
+                         prologue=ww.PRO_MUL)
+    with pytest.raises(ww.WWError) as e:
+        ww.Program([[mul_no_x2]])
+    assert e.value.status == ww.ERR_INVALID_ARGUMENT
+    misaligned = ww.Stage(packed=pk[1:], scales=sc, n_local=16, row0=0, m=2048, x=x, y=[y], wait=0)
+    with pytest.raises(ww.WWError) as e:
+        ww.Program([[misaligned]])
+    assert e.value.status == ww.ERR_MISALIGNED
