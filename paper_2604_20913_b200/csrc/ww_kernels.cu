@@ -289,6 +289,13 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     trace(tslot, 0);
     trace(tslot, 30);
     pdl_launch_dependents();
+    // the x tensor maps' descriptors into the TMA unit's cache before the wait (they do not
+    // depend on the previous kernel), so the first box after the wait does not fetch them
+    if (single && p.use_tma && threadIdx.x == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap)) : "memory");
+        if (p.pro == WW_PRO_MUL)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap2)) : "memory");
+    }
 #if WW_DEBUG_FLAGS
     if (threadIdx.x == 0 && (p.dbg & 8)) {
         const char* wb = reinterpret_cast<const char*>(p.packed + r0 * p.W);

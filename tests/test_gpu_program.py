@@ -121,12 +121,12 @@ def _check_stage(got, want, scales, x_eff, tag):
     assert rel <= 1e-5 and worst <= 1.0, (tag, rel, worst)
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_decode_block_matches_oracle_stage_by_stage(world):
+@pytest.mark.parametrize("world,conv", [(1, 0), (2, 0), (1, 1)])
+def test_decode_block_matches_oracle_stage_by_stage(world, conv):
     layers = 2
     gam_h = block_gammas(0, layers, 2048)
     gam = [tuple(torch.from_numpy(g).cuda() for g in pair) for pair in gam_h]
-    parts = [WLStack(layers=layers, seed=0, rank=r, world=world) for r in range(world)]
+    parts = [WLStack(layers=layers, seed=0, rank=r, world=world, conv=conv) for r in range(world)]
     prog = ww.Program([program_stages(p, parts, "block", gam) for p in parts], world=world)
     prog.run()
     torch.cuda.synchronize()
@@ -147,18 +147,18 @@ def test_decode_block_matches_oracle_stage_by_stage(world):
         xa = orc.rmsnorm(h, gam_h[l][0])
         for name, lo in (("q", 0), ("k", 2048), ("v", 4096)):
             (UW, sc), _ = dense[name]
-            _check_stage(qkv[lo:lo + 2048], orc.wl_dense_apply(*UW, xa), sc, xa, f"L{l}.{name}")
+            _check_stage(qkv[lo:lo + 2048], orc.wl_dense_apply(*UW, xa, conv), sc, xa, f"L{l}.{name}")
         v = qkv[4096:6144]
         (UW, sc), _ = dense["o"]
-        _check_stage(h1, orc.wl_dense_apply(*UW, v) + h, sc, v, f"L{l}.o")
+        _check_stage(h1, orc.wl_dense_apply(*UW, v, conv) + h, sc, v, f"L{l}.o")
         xm = orc.rmsnorm(h1, gam_h[l][1])
         (UW, sc), _ = dense["gate"]
-        _check_stage(gu[:5504], orc.silu_c(orc.wl_dense_apply(*UW, xm)), sc, xm, f"L{l}.gate")
+        _check_stage(gu[:5504], orc.silu_c(orc.wl_dense_apply(*UW, xm, conv)), sc, xm, f"L{l}.gate")
         (UW, sc), _ = dense["up"]
-        _check_stage(gu[5504:11008], orc.wl_dense_apply(*UW, xm), sc, xm, f"L{l}.up")
+        _check_stage(gu[5504:11008], orc.wl_dense_apply(*UW, xm, conv), sc, xm, f"L{l}.up")
         a = orc.mul_c(gu[:5504], gu[5504:11008])
         (UW, sc), _ = dense["down"]
-        _check_stage(h2, orc.wl_dense_apply(*UW, a) + h1, sc, a, f"L{l}.down")
+        _check_stage(h2, orc.wl_dense_apply(*UW, a, conv) + h1, sc, a, f"L{l}.down")
     # end to end over the two blocks from h0, fp64 oracle all the way (<= 1e-3)
     h = h0.astype(np.complex128)
     for l in range(layers):
@@ -166,7 +166,7 @@ def test_decode_block_matches_oracle_stage_by_stage(world):
         for st in P.stages[4 * l:4 * l + 4]:
             for mb in st.members:
                 layer[ww.stack.PROJ_NAMES[mb.proj]] = _dense_layer(P, st, mb)[0]
-        h, _ = orc.block_forward(layer, h, gam_h[l])
+        h, _ = orc.block_forward(layer, h, gam_h[l], conv=conv)
     rel = np.linalg.norm(Y[-1] - h) / np.linalg.norm(h)
     assert rel <= 1e-5, rel
 
