@@ -303,6 +303,8 @@ def run_ours(args, world, rank, local):
         workload = f"{spec.name} x {stack.R} rotating replicas (>= 4x L2)"
 
     s = torch.cuda.Stream(dev)
+    if args.x_l2_persist:  # the step's activations stay in L2 while the weights stream past
+        ww.keep_in_l2(stack.inputs(), s)
     launches_per_step = 0
     with torch.cuda.stream(s):
         for _ in range(max(args.warmup, 3)):
@@ -448,6 +450,7 @@ def run_ours(args, world, rank, local):
                    "parallelism": f"rows/{world} + NCCL all-gather" if world > 1 else "1 GPU",
                    "graph": graph is not None, "pdl": not args.no_pdl,
                    "nccl_in_graph": bool(graph is not None and world > 1),
+                   "x_l2_persist": bool(args.x_l2_persist),
                    "l2": "inputs > L2: 1.62 GB of weights per step streamed from HBM"
                          if args.workload == "c4" else "rotating replicas >= 4x L2",
                    "launch": _launch_configs(ww, stack, args)},
@@ -691,6 +694,10 @@ def main():
                     help="c4: PDL-chained launches per stage, or one persistent program launch")
     ap.add_argument("--chain", choices=("plain", "block"), default="plain",
                     help="c4 program: independent seeded stage inputs, or NEXT-3 decode blocks")
+    ap.add_argument("--no-x-l2-persist", dest="x_l2_persist", action="store_false",
+                    help="do not keep the step's input activations persisting in L2 (default: keep "
+                         "them, ww_stream_keep_in_l2, so the H2D-fed inputs of the e2e leg stay "
+                         "L2-resident while the weights stream)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")

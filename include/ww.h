@@ -263,6 +263,13 @@ ww_status ww_program_init(const ww_stage* stages, int32_t nstages, int32_t world
  * Every rank must launch the same program the same number of times. */
 ww_status ww_program_run(const ww_program* prog, void* stream);
 
+/* Keep [ptr, ptr + bytes) persisting in L2 for kernels launched on `stream` (and kernel nodes
+ * captured from it): access-policy window, hit ratio 1, streaming misses; reserves up to
+ * `bytes` of persisting L2 (device maximum).  For activations every CTA re-reads while the
+ * packed weights stream past.  bytes == 0 clears the window.  WW_ERR_UNSUPPORTED without
+ * persisting L2, WW_ERR_CUDA if the runtime refuses. */
+ww_status ww_stream_keep_in_l2(void* stream, const void* ptr, size_t bytes);
+
 const char* ww_status_string(ww_status s);
 const char* ww_last_error(void); /* thread-local message of the last failing call */
 int32_t ww_version(void);

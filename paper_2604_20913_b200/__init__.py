@@ -43,7 +43,7 @@ EXPORTS = ("ww_packed_bytes", "ww_pack_ternary", "ww_unpack_ternary", "ww_repack
            "ww_pack_ternary_device", "ww_wl_gemv", "ww_wl_gemv_batched", "ww_shard_plan",
            "ww_query_launch", "ww_status_string", "ww_last_error", "ww_version",
            "ww_ternary_gemv_plane", "ww_wl_combine", "ww_wl_gemv_fused", "ww_program_workspace_bytes",
-           "ww_program_sync_bytes", "ww_program_init", "ww_program_run")
+           "ww_program_sync_bytes", "ww_program_init", "ww_program_run", "ww_stream_keep_in_l2")
 
 
 class WWError(RuntimeError):
@@ -132,6 +132,8 @@ _lib.ww_program_init.argtypes = [ctypes.POINTER(_Stage), _i32, _i32, _i32, _i32,
                                  ctypes.POINTER(_vp), _vp, ctypes.POINTER(_Program)]
 _lib.ww_program_run.restype = _i32
 _lib.ww_program_run.argtypes = [ctypes.POINTER(_Program), _vp]
+_lib.ww_stream_keep_in_l2.restype = _i32
+_lib.ww_stream_keep_in_l2.argtypes = [_vp, _vp, ctypes.c_size_t]
 _lib.ww_status_string.restype = ctypes.c_char_p
 _lib.ww_status_string.argtypes = [_i32]
 _lib.ww_last_error.restype = ctypes.c_char_p
@@ -451,3 +453,13 @@ class Program:
 
     def run(self, stream=None):
         _check(_lib.ww_program_run(ctypes.byref(self.prog), _stream_ptr(stream)))
+
+
+def keep_in_l2(tensor, stream=None):
+    """ww_stream_keep_in_l2: keep `tensor` persisting in L2 for launches on `stream` (None:
+    the current stream); tensor=None clears the window."""
+    sp = _stream_ptr(stream)
+    if tensor is None:
+        _check(_lib.ww_stream_keep_in_l2(sp, None, 0))
+    else:
+        _check(_lib.ww_stream_keep_in_l2(sp, tensor.data_ptr(), tensor.numel() * tensor.element_size()))

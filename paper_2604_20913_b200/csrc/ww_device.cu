@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -95,3 +96,37 @@ int encode_x_map(void* map, const float* X, int64_t W, int64_t B, int64_t ldx) {
 }
 
 }  // namespace ww
+
+// Keep [ptr, ptr + bytes) resident in L2 for kernels launched on `stream` (and kernel nodes
+// captured from it): an access-policy window with hit ratio 1 (persisting) and streaming
+// misses, after reserving that much persisting L2 (capped by the device's maximum).  For the
+// activations of a decode step, which every CTA of the next stage re-reads while the weights
+// stream through L2.  bytes == 0 clears the window.
+extern "C" ww_status ww_stream_keep_in_l2(void* stream, const void* ptr, size_t bytes) {
+    cudaStreamAttrValue v;
+    memset(&v, 0, sizeof v);
+    if (bytes) {
+        if (!ptr) return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_stream_keep_in_l2: null pointer");
+        int dev = ww::current_device(), maxp = 0, maxw = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        if (maxp <= 0 || maxw <= 0)
+            return ww::fail(WW_ERR_UNSUPPORTED, "ww_stream_keep_in_l2: no persisting L2 on this device");
+        const size_t want = bytes < (size_t)maxp ? bytes : (size_t)maxp;
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        if (cur < want) {
+            cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            if (e != cudaSuccess)
+                return ww::fail(WW_ERR_CUDA, "ww_stream_keep_in_l2: %s", cudaGetErrorString(e));
+        }
+        v.accessPolicyWindow.base_ptr = const_cast<void*>(ptr);
+        v.accessPolicyWindow.num_bytes = bytes < (size_t)maxw ? bytes : (size_t)maxw;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    }
+    cudaError_t e = cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    if (e != cudaSuccess) return ww::fail(WW_ERR_CUDA, "ww_stream_keep_in_l2: %s", cudaGetErrorString(e));
+    return ww::ok();
+}
