@@ -404,7 +404,10 @@ def run_ours(args, world, rank, local):
             except Exception as e:  # pragma: no cover
                 per_shape[label] = f"unavailable: {e!r}"
             if world > 1:  # the same stages' all-gathers alone (SURVEY §8e breakdown)
-                allgather_us[label] = _time_allgathers(stack, idx, s, dev)
+                try:
+                    allgather_us[label] = _time_allgathers(stack, idx, s, dev)
+                except Exception as e:  # pragma: no cover - multi-GPU only
+                    allgather_us[label] = f"unavailable: {e!r}"
 
     # ---------------- e2e: host activations in, result out, through the same API calls
     e2e = _e2e(stack, args, s, dev, graph, world, alg_bytes)

@@ -375,3 +375,16 @@ def test_pdl_chain_reads_previous_layers_output(B, graph):
         torch.cuda.synchronize()
         for a, b in zip(ref, got):
             assert torch.equal(torch.view_as_real(a), torch.view_as_real(b))
+
+
+def test_keep_in_l2_window_leaves_results_unchanged():
+    # ww_stream_keep_in_l2 only changes caching: same bits with and without the window
+    case = LayerCase.from_spec(wi.C2, seed=4).device(ww, torch)
+    s = torch.cuda.Stream()
+    L = case.layer(ww, ww.CONV_EQ1)
+    y0 = ww.wl_gemv(L, case.packed_d, case.scales_d, case.x_d[0], stream=s)
+    ww.keep_in_l2(case.x_d, s)
+    y1 = ww.wl_gemv(L, case.packed_d, case.scales_d, case.x_d[0], stream=s)
+    ww.keep_in_l2(None, s)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
