@@ -429,6 +429,14 @@ def run_ours(args, world, rank, local):
     achieved_alu = rank_adds / launches / per_launch_s / 1e12
     rank_pa = stack.packed_act_bytes()
     hbm_achieved = rank_pa / launches / per_launch_s / 1e9
+    if getattr(stack, "tc", False):  # tcgen05 kind::i8: MACs of the padded contraction
+        macs = stack.R * 4 * stack.nloc * (ww.tc_workspace_bytes(stack.spec.m, stack.B) - 256)
+        tops = 2 * macs / launches / per_launch_s / 1e12
+        i8_peak = 2 * peaks.get("bf16_tflops", 1622.9)  # int8 = 2x the measured bf16 rate
+        tc_roof = {"bound": "tensor", "achieved": round(tops, 2), "peak": round(i8_peak, 1),
+                   "unit": "TOPS (int8)", "frac": round(tops / i8_peak, 4),
+                   "kernel": "wl_tc_kernel (tcgen05.mma kind::i8)",
+                   "peak_basis": "measured bf16 TFLOP/s x 2 (int8 nominal ratio)"}
     roof = {"bound": "alu", "achieved": round(achieved_alu, 4), "peak": round(alu_peak, 4),
             "unit": "Tadd/s", "frac": round(achieved_alu / alu_peak, 4),
             "traffic": _ncu_traffic(),
@@ -454,6 +462,8 @@ def run_ours(args, world, rank, local):
                    "graph": graph is not None, "pdl": not args.no_pdl,
                    "nccl_in_graph": bool(graph is not None and world > 1),
                    "x_l2_persist": bool(args.x_l2_persist),
+                   "path": ("tcgen05 kind::i8 (wl_tc_kernel)" if getattr(stack, "tc", False)
+                            else "predicated FADD2 (wl_gemv_kernel)"),
                    "l2": "inputs > L2: 1.62 GB of weights per step streamed from HBM"
                          if args.workload == "c4" else "rotating replicas >= 4x L2",
                    "launch": _launch_configs(ww, stack, args)},
@@ -465,7 +475,7 @@ def run_ours(args, world, rank, local):
                                  / peaks.get("hbm_gbs", 6650.0), 2),
         "hbm_frac": roof["hbm"]["frac"],
         "alu_frac": roof["frac"],
-        "roofline": roof,
+        "roofline": tc_roof if getattr(stack, "tc", False) else roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
@@ -627,6 +637,10 @@ class _ReplicaLayer:
         self.L = ww.Layer(self.nloc, spec.m, ww.LAYOUT_COL4,
                           ww.SCALES_PER_ROW if spec.per_row else ww.SCALES_PER_TENSOR,
                           ww.CONV_EQ1, 0 if args.no_pdl else ww.FLAG_PDL)
+        # batches of >= 4 vectors run on the tensor cores (ww_wl_gemv_batched_tc) unless --no-tc
+        self.tc = (not args.no_tc) and self.B >= 4 and ww.tc_workspace_bytes(spec.m, self.B) > 0
+        self.ws = (torch.empty(ww.tc_workspace_bytes(spec.m, self.B) + 256, dtype=torch.uint8, device=dev)
+                   if self.tc else None)
 
     def inputs(self):
         return self.X
@@ -635,7 +649,10 @@ class _ReplicaLayer:
         rpr = self.shard.rows_per_rank
         yv = self.Y[0][self.rank * self.B * rpr:(self.rank + 1) * self.B * rpr].view(self.B, rpr)
         for r in range(self.R):
-            self.ww.wl_gemv_batched(self.L, self.Wr[r], self.S, self.X, yv, stream=s)
+            if self.tc:  # the batch as a dense contraction on the tensor cores
+                self.ww.wl_gemv_batched_tc(self.L, self.Wr[r], self.S, self.X, yv, self.ws, stream=s)
+            else:
+                self.ww.wl_gemv_batched(self.L, self.Wr[r], self.S, self.X, yv, stream=s)
             if self.world > 1:
                 import torch.distributed as dist
                 n = self.Y[0].numel() // self.world
@@ -705,6 +722,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tc", action="store_true",
+                    help="single-layer workloads: keep B >= 4 on the predicated-FADD2 kernel instead "
+                         "of the tcgen05 path")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3

@@ -263,6 +263,22 @@ ww_status ww_program_init(const ww_stage* stages, int32_t nstages, int32_t world
  * Every rank must launch the same program the same number of times. */
 ww_status ww_program_run(const ww_program* prog, void* stream);
 
+/* Batched WL-GEMV on the tensor cores (tcgen05.mma kind::i8) for the small-batch variant
+ * (BASELINE config 5): with B vectors the layer is a dense contraction of the stacked ternary
+ * planes (4n x m, decoded in-kernel from COL4 to int8 in shared memory) with the B x 2 real
+ * components of x, each split into three signed 8-bit limbs of a 22-bit fixed-point value
+ * (scale 2^-E per vector and component, E from max |x|); int32 accumulation is exact, the
+ * limbs are recombined in fp64 and the scales applied once per row (Eq. 1 /
+ * Eqs. 2-3).  Error: x's 22-bit grid relative to max |x| of its vector and component.
+ * X: B rows of m complex64 (stride ldx), Y: B rows of n complex64 (stride ldy); 1 <= B <= 16,
+ * m <= 11264 (each x component is staged in shared memory to split it).
+ * workspace_d: ww_tc_workspace_bytes(m, B) bytes, 128-B aligned, caller-owned (limbs and
+ * exponents, rewritten every call).  Two launches on `stream` (limbs, then the MMA kernel). */
+size_t ww_tc_workspace_bytes(int64_t m, int32_t B);
+ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed_d, const float* scales_d,
+                                const float* X_d, int64_t ldx, float* Y_d, int64_t ldy, int32_t B,
+                                void* workspace_d, void* stream);
+
 /* Keep [ptr, ptr + bytes) persisting in L2 for kernels launched on `stream` (and kernel nodes
  * captured from it): access-policy window, hit ratio 1, streaming misses; reserves up to
  * `bytes` of persisting L2 (device maximum).  For activations every CTA re-reads while the

@@ -43,7 +43,8 @@ EXPORTS = ("ww_packed_bytes", "ww_pack_ternary", "ww_unpack_ternary", "ww_repack
            "ww_pack_ternary_device", "ww_wl_gemv", "ww_wl_gemv_batched", "ww_shard_plan",
            "ww_query_launch", "ww_status_string", "ww_last_error", "ww_version",
            "ww_ternary_gemv_plane", "ww_wl_combine", "ww_wl_gemv_fused", "ww_program_workspace_bytes",
-           "ww_program_sync_bytes", "ww_program_init", "ww_program_run", "ww_stream_keep_in_l2")
+           "ww_program_sync_bytes", "ww_program_init", "ww_program_run", "ww_stream_keep_in_l2",
+           "ww_tc_workspace_bytes", "ww_wl_gemv_batched_tc")
 
 
 class WWError(RuntimeError):
@@ -132,6 +133,11 @@ _lib.ww_program_init.argtypes = [ctypes.POINTER(_Stage), _i32, _i32, _i32, _i32,
                                  ctypes.POINTER(_vp), _vp, ctypes.POINTER(_Program)]
 _lib.ww_program_run.restype = _i32
 _lib.ww_program_run.argtypes = [ctypes.POINTER(_Program), _vp]
+_lib.ww_tc_workspace_bytes.restype = ctypes.c_size_t
+_lib.ww_tc_workspace_bytes.argtypes = [_i64, _i32]
+_lib.ww_wl_gemv_batched_tc.restype = _i32
+_lib.ww_wl_gemv_batched_tc.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _i64, _vp, _i64, _i32,
+                                       _vp, _vp]
 _lib.ww_stream_keep_in_l2.restype = _i32
 _lib.ww_stream_keep_in_l2.argtypes = [_vp, _vp, ctypes.c_size_t]
 _lib.ww_status_string.restype = ctypes.c_char_p
@@ -463,3 +469,29 @@ def keep_in_l2(tensor, stream=None):
         _check(_lib.ww_stream_keep_in_l2(sp, None, 0))
     else:
         _check(_lib.ww_stream_keep_in_l2(sp, tensor.data_ptr(), tensor.numel() * tensor.element_size()))
+
+
+def tc_workspace_bytes(m: int, B: int) -> int:
+    return int(_lib.ww_tc_workspace_bytes(m, B))
+
+
+def wl_gemv_batched_tc(layer: Layer, packed, scales, X, Y=None, workspace=None, stream=None):
+    """Y[b] = WL-GEMV(X[b]) on the tensor cores (ww_wl_gemv_batched_tc; 1 <= B <= 16)."""
+    import torch
+    B = X.shape[0]
+    if Y is None:
+        Y = torch.empty((B, layer.n), dtype=torch.complex64, device=X.device)
+    if X.dim() != 2 or Y.dim() != 2:
+        raise ValueError("X and Y must be 2-D (B, m) / (B, n) tensors")
+    _check_args(layer, packed, scales, X, Y, B)
+    nb = tc_workspace_bytes(layer.m, B)
+    if nb == 0:
+        raise ValueError(f"batch {B} unsupported by the tensor-core path (1..16)")
+    if workspace is None or workspace.numel() * workspace.element_size() < nb + 128:
+        workspace = torch.empty(nb + 128, dtype=torch.uint8, device=X.device)
+    wp = (workspace.data_ptr() + 127) // 128 * 128
+    L = layer.c()
+    _check(_lib.ww_wl_gemv_batched_tc(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(),
+                                      X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0), B, wp,
+                                      _stream_ptr(stream)))
+    return Y
