@@ -22,6 +22,13 @@
  *     bit 2p+1 = (plane p code == +1), bit 2p = (plane p code == -1), p = 0..3 =
  *     U_re, U_im, W_re, W_im.  Same 2 bits per code (n*W*16 bytes = n*m when 16 | m);
  *     the bit order is chosen so one R2P decodes a column's predicates.
+ *   WW_LAYOUT_TILE32 (device layout of the tensor-core path, ww_wl_gemv_tc): the App. H
+ *     words themselves, re-tiled.  Rows are grouped in tiles of 32, columns in slabs of 64
+ *     (4 words), S = ceil(W/4); the 512 words of (tile t, slab s) are contiguous, M-row
+ *     major: word index ((t*S + s)*128 + 4*(i%32) + p)*4 + (w%4) holds App. H word w of
+ *     plane p, row i (t = i/32, s = w/4).  Rows past n and words past W are zero codes.
+ *     ww_packed_bytes_layout(): ceil(n/32) * S * 2048 bytes (2 bits per code, the same bytes
+ *     as the other layouts when 32 | n and 64 | m).
  *
  * Scales (R2): WW_SCALES_PER_ROW = n x 4 fp32 [sUr, sUi, sWr, sWi] row-major;
  *   WW_SCALES_PER_TENSOR = 4 fp32 shared by all rows.
@@ -58,7 +65,7 @@ typedef enum {
     WW_ERR_CUDA = 8                /* a CUDA runtime call failed; see ww_last_error() */
 } ww_status;
 
-typedef enum { WW_LAYOUT_PLANAR = 0, WW_LAYOUT_COL4 = 1 } ww_layout;
+typedef enum { WW_LAYOUT_PLANAR = 0, WW_LAYOUT_COL4 = 1, WW_LAYOUT_TILE32 = 2 } ww_layout;
 typedef enum { WW_CONV_EQ1 = 0, WW_CONV_ALG1 = 1 } ww_convention;
 typedef enum { WW_SCALES_PER_TENSOR = 0, WW_SCALES_PER_ROW = 1 } ww_scale_mode;
 
@@ -81,12 +88,17 @@ typedef struct {
     uint32_t flags;     /* WW_FLAG_* */
 } ww_layer;
 
-/* Bytes of packed weights for an n x m layer in either layout: 16 * n * ceil(m/16). */
+/* Bytes of packed weights for an n x m layer in WW_LAYOUT_PLANAR or WW_LAYOUT_COL4:
+ * 16 * n * ceil(m/16). */
 size_t ww_packed_bytes(int64_t n, int64_t m);
+/* Bytes of packed weights in any layout (WW_LAYOUT_TILE32: ceil(n/32) * ceil(m/64) * 2048);
+ * 0 for an unknown layout or negative sizes. */
+size_t ww_packed_bytes_layout(int64_t n, int64_t m, int32_t layout);
 
 /* Host packer (App. H).  u_re..w_im: dense int8 n x m planes, row stride ld
  * (>= m) elements; values must be in {-1,0,+1} (else WW_ERR_INVALID_CODE, nothing
- * promised about `out`).  out: ww_packed_bytes(n,m) bytes, caller-owned host memory. */
+ * promised about `out`).  out: ww_packed_bytes_layout(n,m,layout) bytes, caller-owned host
+ * memory.  Every layout (PLANAR, COL4, TILE32) is accepted by the three host functions. */
 ww_status ww_pack_ternary(const int8_t* u_re, const int8_t* u_im, const int8_t* w_re,
                           const int8_t* w_im, int64_t n, int64_t m, int64_t ld, int32_t layout,
                           uint32_t* out);
@@ -95,7 +107,7 @@ ww_status ww_pack_ternary(const int8_t* u_re, const int8_t* u_im, const int8_t* 
 ww_status ww_unpack_ternary(const uint32_t* packed, int64_t n, int64_t m, int32_t layout,
                             int8_t* u_re, int8_t* u_im, int8_t* w_re, int8_t* w_im, int64_t ld);
 
-/* Host re-layout between WW_LAYOUT_PLANAR and WW_LAYOUT_COL4 (src and dst distinct). */
+/* Host re-layout between any two layouts (src and dst distinct; sizes per layout). */
 ww_status ww_repack(const uint32_t* src, int32_t src_layout, int64_t n, int64_t m,
                     uint32_t* dst, int32_t dst_layout);
 
@@ -106,6 +118,12 @@ ww_status ww_repack(const uint32_t* src, int32_t src_layout, int64_t n, int64_t 
  * as zero); it is never cleared by the library.  Asynchronous on `stream`. */
 ww_status ww_pack_ternary_device(const int8_t* planes_d, int64_t n, int64_t m, int64_t ld,
                                  uint32_t* out_d, int32_t* bad_d, void* stream);
+/* The same device packer for any GPU layout: WW_LAYOUT_COL4 (== ww_pack_ternary_device) or
+ * WW_LAYOUT_TILE32 (out_d: ww_packed_bytes_layout(n,m,WW_LAYOUT_TILE32) bytes, 16-B aligned;
+ * an invalid value packs its 16-column word of that plane as zero and sets *bad_d). */
+ww_status ww_pack_ternary_device_layout(const int8_t* planes_d, int64_t n, int64_t m, int64_t ld,
+                                        int32_t layout, uint32_t* out_d, int32_t* bad_d,
+                                        void* stream);
 
 /* Fused WL-GEMV, one vector (B = 1).  packed_d: WW_LAYOUT_COL4, 16-B aligned;
  * scales_d: per row n x 4 or per tensor 4 fp32; x_d: m complex64; y_d: n complex64
@@ -278,6 +296,29 @@ size_t ww_tc_workspace_bytes(int64_t m, int32_t B);
 ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed_d, const float* scales_d,
                                 const float* X_d, int64_t ldx, float* Y_d, int64_t ldy, int32_t B,
                                 void* workspace_d, void* stream);
+
+/* WL-GEMV on the tensor cores with the ternary operand decoded into tensor memory (B = 1..4;
+ * DESIGN.md §6 "wl_tcv_kernel").  The eight real sub-GEMVs of Eq. 1 (Eqs. 6-7,
+ * P:931-946) are one exact integer contraction per 32-row tile: the App. H words
+ * (WW_LAYOUT_TILE32, read once from HBM) are expanded in-kernel to int8 {-1, 0, +1} in tensor
+ * memory, each real component of x is an offset 22-bit fixed-point value 2^22 + rint(x 2^E)
+ * (E = 20 - ilogb(max |x|) per vector and component) split into three unsigned bytes, and
+ * tcgen05.mma kind::i8 accumulates in int32 (exact); the scales are applied once per row
+ * after accumulation with the EQ1 / ALG1 signs.  Error: x's grid 2^-E (about
+ * max|x| 2^-21) and the final fp64 -> fp32 rounding; results are bitwise independent of the
+ * grid and of the row shard.  x must be finite.
+ * L->layout must be WW_LAYOUT_TILE32 (packed_d: ww_packed_bytes_layout(n, m, TILE32) bytes,
+ * 16-B aligned); X: B rows of m complex64 (stride ldx >= m, 8-B aligned), Y: B rows of n
+ * complex64 (stride ldy >= n); x and y must not overlap.  WW_FLAG_PDL as for ww_wl_gemv (the
+ * weights are read before griddepcontrol.wait, x / scales / y / workspace after it).
+ * workspace_d: ww_tcv_workspace_bytes(n, m, B) bytes, 16-B aligned, caller-owned, ZEROED
+ * before its first use; every call leaves it zeroed again (split tiles reduce their int32
+ * partial sums there), so launches sharing one workspace must be stream-ordered.
+ * Errors: WW_ERR_UNSUPPORTED (layout, B > 4, x's slabs beyond shared memory), the usual
+ * argument / alignment errors before any launch.  One launch on `stream`. */
+size_t ww_tcv_workspace_bytes(int64_t n, int64_t m, int32_t B);
+ww_status ww_wl_gemv_tc(const ww_layer* L, const void* packed_d, const float* scales_d, const float* X_d,
+                        int64_t ldx, float* Y_d, int64_t ldy, int32_t B, void* workspace_d, void* stream);
 
 /* Keep [ptr, ptr + bytes) persisting in L2 for kernels launched on `stream` (and kernel nodes
  * captured from it): access-policy window, hit ratio 1, streaming misses; reserves up to

@@ -27,7 +27,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 OK = 0
 ERR_INVALID_ARGUMENT, ERR_DIMENSION_MISMATCH, ERR_INVALID_CODE, ERR_INVALID_ENCODING = 1, 2, 3, 4
 ERR_NONFINITE_SCALE, ERR_MISALIGNED, ERR_UNSUPPORTED, ERR_CUDA = 5, 6, 7, 8
-LAYOUT_PLANAR, LAYOUT_COL4 = 0, 1
+LAYOUT_PLANAR, LAYOUT_COL4, LAYOUT_TILE32 = 0, 1, 2
 CONV_EQ1, CONV_ALG1 = 0, 1
 SCALES_PER_TENSOR, SCALES_PER_ROW = 0, 1
 FLAG_PDL = 1
@@ -44,7 +44,8 @@ EXPORTS = ("ww_packed_bytes", "ww_pack_ternary", "ww_unpack_ternary", "ww_repack
            "ww_query_launch", "ww_status_string", "ww_last_error", "ww_version",
            "ww_ternary_gemv_plane", "ww_wl_combine", "ww_wl_gemv_fused", "ww_program_workspace_bytes",
            "ww_program_sync_bytes", "ww_program_init", "ww_program_run", "ww_stream_keep_in_l2",
-           "ww_tc_workspace_bytes", "ww_wl_gemv_batched_tc")
+           "ww_tc_workspace_bytes", "ww_wl_gemv_batched_tc", "ww_packed_bytes_layout",
+           "ww_pack_ternary_device_layout", "ww_tcv_workspace_bytes", "ww_wl_gemv_tc")
 
 
 class WWError(RuntimeError):
@@ -138,6 +139,14 @@ _lib.ww_tc_workspace_bytes.argtypes = [_i64, _i32]
 _lib.ww_wl_gemv_batched_tc.restype = _i32
 _lib.ww_wl_gemv_batched_tc.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _i64, _vp, _i64, _i32,
                                        _vp, _vp]
+_lib.ww_packed_bytes_layout.restype = ctypes.c_size_t
+_lib.ww_packed_bytes_layout.argtypes = [_i64, _i64, _i32]
+_lib.ww_pack_ternary_device_layout.restype = _i32
+_lib.ww_pack_ternary_device_layout.argtypes = [_vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp]
+_lib.ww_tcv_workspace_bytes.restype = ctypes.c_size_t
+_lib.ww_tcv_workspace_bytes.argtypes = [_i64, _i64, _i32]
+_lib.ww_wl_gemv_tc.restype = _i32
+_lib.ww_wl_gemv_tc.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]
 _lib.ww_stream_keep_in_l2.restype = _i32
 _lib.ww_stream_keep_in_l2.argtypes = [_vp, _vp, ctypes.c_size_t]
 _lib.ww_status_string.restype = ctypes.c_char_p
@@ -180,7 +189,9 @@ class Layer:
         return _Layer(self.n, self.m, self.layout, self.scale_mode, self.conv, self.flags)
 
 
-def packed_bytes(n: int, m: int) -> int:
+def packed_bytes(n: int, m: int, layout: int = LAYOUT_COL4) -> int:
+    if layout == LAYOUT_TILE32:
+        return int(_lib.ww_packed_bytes_layout(n, m, layout))
     return int(_lib.ww_packed_bytes(n, m))
 
 
@@ -189,7 +200,7 @@ def pack_ternary(planes: np.ndarray, layout: int = LAYOUT_COL4) -> np.ndarray:
     """(4, n, m) int8 planes U_re, U_im, W_re, W_im -> packed uint32 words (host)."""
     p = np.ascontiguousarray(planes, dtype=np.int8)
     _, n, m = p.shape
-    out = np.empty(packed_bytes(n, m) // 4, dtype=np.uint32)
+    out = np.empty(packed_bytes(n, m, layout) // 4, dtype=np.uint32)
     _check(_lib.ww_pack_ternary(p[0].ctypes.data, p[1].ctypes.data, p[2].ctypes.data,
                                 p[3].ctypes.data, n, m, m, layout, out.ctypes.data))
     return out
@@ -197,7 +208,7 @@ def pack_ternary(planes: np.ndarray, layout: int = LAYOUT_COL4) -> np.ndarray:
 
 def unpack_ternary(packed: np.ndarray, n: int, m: int, layout: int = LAYOUT_COL4) -> np.ndarray:
     w = np.ascontiguousarray(packed, dtype=np.uint32)
-    assert w.nbytes == packed_bytes(n, m)
+    assert w.nbytes == packed_bytes(n, m, layout)
     out = np.empty((4, n, m), dtype=np.int8)
     _check(_lib.ww_unpack_ternary(w.ctypes.data, n, m, layout, out[0].ctypes.data,
                                   out[1].ctypes.data, out[2].ctypes.data, out[3].ctypes.data, m))
@@ -206,7 +217,8 @@ def unpack_ternary(packed: np.ndarray, n: int, m: int, layout: int = LAYOUT_COL4
 
 def repack(packed: np.ndarray, n: int, m: int, src_layout: int, dst_layout: int) -> np.ndarray:
     w = np.ascontiguousarray(packed, dtype=np.uint32)
-    out = np.empty_like(w)
+    assert w.nbytes == packed_bytes(n, m, src_layout)
+    out = np.empty(packed_bytes(n, m, dst_layout) // 4, dtype=np.uint32)
     _check(_lib.ww_repack(w.ctypes.data, src_layout, n, m, out.ctypes.data, dst_layout))
     return out
 
@@ -218,17 +230,21 @@ def _stream_ptr(stream):
     return s.cuda_stream
 
 
-def pack_ternary_device(planes, bad=None, stream=None, out=None):
-    """(4, n, ld) int8 CUDA tensor -> COL4 packed uint8 CUDA tensor of packed_bytes(n, m)."""
+def pack_ternary_device(planes, bad=None, stream=None, out=None, layout: int = LAYOUT_COL4):
+    """(4, n, ld) int8 CUDA tensor -> packed uint8 CUDA tensor of packed_bytes(n, m, layout)
+    (COL4 for the CUDA-core kernels, TILE32 for the tensor-core path)."""
     import torch
     assert planes.is_cuda and planes.dtype == torch.int8 and planes.is_contiguous()
     _, n, ld = planes.shape
     m = ld
+    nb = packed_bytes(n, m, layout)
     if out is None:
-        out = torch.empty(packed_bytes(n, m), dtype=torch.uint8, device=planes.device)
-    _check(_lib.ww_pack_ternary_device(planes.data_ptr(), n, m, ld, out.data_ptr(),
-                                       bad.data_ptr() if bad is not None else None,
-                                       _stream_ptr(stream)))
+        out = torch.empty(nb, dtype=torch.uint8, device=planes.device)
+    if out.numel() * out.element_size() < nb:
+        raise ValueError(f"out has {out.numel() * out.element_size()} bytes, needs {nb}")
+    _check(_lib.ww_pack_ternary_device_layout(planes.data_ptr(), n, m, ld, layout, out.data_ptr(),
+                                              bad.data_ptr() if bad is not None else None,
+                                              _stream_ptr(stream)))
     return out
 
 
@@ -254,8 +270,9 @@ def _check_args(layer: Layer, packed, scales, X, Y, B: int):
     need = 4 * layer.n if layer.scale_mode == SCALES_PER_ROW else 4
     if scales.numel() < need:
         raise ValueError(f"scales has {scales.numel()} floats, needs {need}")
-    if not packed.is_contiguous() or packed.numel() * packed.element_size() < packed_bytes(layer.n, layer.m):
-        raise ValueError(f"packed must be contiguous with >= {packed_bytes(layer.n, layer.m)} bytes")
+    need = packed_bytes(layer.n, layer.m, layer.layout)
+    if not packed.is_contiguous() or packed.numel() * packed.element_size() < need:
+        raise ValueError(f"packed must be contiguous with >= {need} bytes")
 
 
 def wl_gemv(layer: Layer, packed, scales, x, y=None, stream=None):
@@ -494,4 +511,47 @@ def wl_gemv_batched_tc(layer: Layer, packed, scales, X, Y=None, workspace=None, 
     _check(_lib.ww_wl_gemv_batched_tc(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(),
                                       X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0), B, wp,
                                       _stream_ptr(stream)))
+    return Y
+
+
+def tcv_workspace_bytes(n: int, m: int, B: int = 1) -> int:
+    """Bytes of the zero-initialised workspace ww_wl_gemv_tc needs (0: unsupported B)."""
+    return int(_lib.ww_tcv_workspace_bytes(n, m, B))
+
+
+def tcv_workspace(n: int, m: int, B: int = 1, device=None):
+    """A zeroed workspace for ww_wl_gemv_tc (every call leaves it zeroed again)."""
+    import torch
+    nb = tcv_workspace_bytes(n, m, B)
+    if nb == 0:
+        raise ValueError(f"batch {B} unsupported by ww_wl_gemv_tc (1..4)")
+    return torch.zeros(nb, dtype=torch.uint8, device=device if device is not None else "cuda")
+
+
+def wl_gemv_tc(layer: Layer, packed, scales, X, Y=None, workspace=None, stream=None):
+    """Y[b] = WL-GEMV(X[b]) on the tensor cores (ww_wl_gemv_tc; TILE32 weights, 1 <= B <= 4).
+    X may be a (B, m) or an (m,) complex64 CUDA tensor; Y has the same rank."""
+    import torch
+    vec = X.dim() == 1
+    X2 = X.view(1, -1) if vec else X
+    B = X2.shape[0]
+    if Y is None:
+        Y = torch.empty((B, layer.n) if not vec else (layer.n,), dtype=torch.complex64, device=X.device)
+    Y2 = Y.view(1, -1) if Y.dim() == 1 else Y
+    if X2.dim() != 2 or Y2.dim() != 2:
+        raise ValueError("X and Y must be (B, m) / (B, n) or 1-D tensors")
+    if layer.layout != LAYOUT_TILE32:
+        raise ValueError("wl_gemv_tc needs layout LAYOUT_TILE32")
+    _check_args(layer, packed, scales, X2, Y2, B)
+    nb = tcv_workspace_bytes(layer.n, layer.m, B)
+    if nb == 0:
+        raise ValueError(f"batch {B} unsupported by the tensor-core path (1..4)")
+    if workspace is None:
+        workspace = tcv_workspace(layer.n, layer.m, B, X.device)
+    if workspace.numel() * workspace.element_size() < nb or workspace.data_ptr() % 16:
+        raise ValueError(f"workspace needs {nb} zeroed, 16-B aligned bytes")
+    L = layer.c()
+    _check(_lib.ww_wl_gemv_tc(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(), X2.data_ptr(),
+                              X2.stride(0), Y2.data_ptr(), Y2.stride(0), B, workspace.data_ptr(),
+                              _stream_ptr(stream)))
     return Y

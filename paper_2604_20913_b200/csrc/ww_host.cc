@@ -52,6 +52,14 @@ extern "C" size_t ww_packed_bytes(int64_t n, int64_t m) {
     return (size_t)16 * (size_t)n * (size_t)ww::words_per_row(m);
 }
 
+extern "C" size_t ww_packed_bytes_layout(int64_t n, int64_t m, int32_t layout) {
+    if (n < 0 || m < 0) return 0;
+    if (layout == WW_LAYOUT_PLANAR || layout == WW_LAYOUT_COL4) return ww_packed_bytes(n, m);
+    if (layout == WW_LAYOUT_TILE32)
+        return (size_t)ww::tile32_tiles(n) * (size_t)ww::tile32_slabs(m) * 2048u;
+    return 0;
+}
+
 namespace {
 
 // 2-bit code of value t (App. H): +1 -> 0b10, -1 -> 0b01, 0 -> 0b00
@@ -76,13 +84,17 @@ inline void locate(int32_t layout, int64_t n, int64_t W, int64_t i, int64_t j, i
     if (layout == WW_LAYOUT_PLANAR) {
         *word = ((int64_t)p * n + i) * W + c;
         *shift = 2 * k;
+    } else if (layout == WW_LAYOUT_TILE32) {  // App. H word c of (p, i), re-tiled (ww.h)
+        const int64_t S = (W + 3) / 4;
+        *word = (((i >> 5) * S + (c >> 2)) * 128 + 4 * (i & 31) + p) * 4 + (c & 3);
+        *shift = 2 * k;
     } else {  // COL4: byte k of the 16-byte chunk (i, c); slot p within the byte
         *word = (i * W + c) * 4 + (k >> 2);
         *shift = 8 * (k & 3) + 2 * p;
     }
 }
 
-bool layout_ok(int32_t l) { return l == WW_LAYOUT_PLANAR || l == WW_LAYOUT_COL4; }
+bool layout_ok(int32_t l) { return l == WW_LAYOUT_PLANAR || l == WW_LAYOUT_COL4 || l == WW_LAYOUT_TILE32; }
 
 }  // namespace
 
@@ -96,7 +108,7 @@ extern "C" ww_status ww_pack_ternary(const int8_t* u_re, const int8_t* u_im, con
                     (long long)n, (long long)m, (long long)ld);
     if (!layout_ok(layout)) return fail(WW_ERR_INVALID_ARGUMENT, "ww_pack_ternary: layout %d", layout);
     const int64_t W = ww::words_per_row(m);
-    std::memset(out, 0, ww_packed_bytes(n, m));  // zero codes everywhere, incl. padding
+    std::memset(out, 0, ww_packed_bytes_layout(n, m, layout));  // zero codes everywhere, incl. padding
     const int8_t* planes[4] = {u_re, u_im, w_re, w_im};
     for (int p = 0; p < 4; ++p) {
         for (int64_t i = 0; i < n; ++i) {
@@ -153,7 +165,7 @@ extern "C" ww_status ww_repack(const uint32_t* src, int32_t src_layout, int64_t 
     if (!layout_ok(src_layout) || !layout_ok(dst_layout))
         return fail(WW_ERR_INVALID_ARGUMENT, "ww_repack: layouts %d -> %d", src_layout, dst_layout);
     const int64_t W = ww::words_per_row(m);
-    std::memset(dst, 0, ww_packed_bytes(n, m));
+    std::memset(dst, 0, ww_packed_bytes_layout(n, m, dst_layout));
     for (int p = 0; p < 4; ++p)
         for (int64_t i = 0; i < n; ++i)
             for (int64_t j = 0; j < 16 * W; ++j) {

@@ -7,6 +7,9 @@
 
 namespace ww {
 inline int64_t words_per_row(int64_t m) { return (m + 15) / 16; }  // 16 codes per word
+// WW_LAYOUT_TILE32 geometry: tiles of 32 rows, slabs of 64 columns (4 words)
+inline int64_t tile32_tiles(int64_t n) { return (n + 31) / 32; }
+inline int64_t tile32_slabs(int64_t m) { return (words_per_row(m) + 3) / 4; }
 ww_status fail(ww_status s, const char* fmt, ...);                  // sets ww_last_error()
 ww_status ok();
 // per-device launch state (ww_device.cu; cached per device, mutex-guarded)

@@ -176,3 +176,58 @@ def test_launch_rows_are_whole_units():
             for n in (1, 148, 2048, 11008):
                 i = ww.query_launch(ww.Layer(n, m), B)
                 assert (i["parts"], i["split_chunks"]) == (1, W)
+
+
+# ---------------------------------------------------------------- WW_LAYOUT_TILE32
+def _tile32_from_app_h(planar, n, m):
+    """Place the oracle's App. H words (4, n, W) at their TILE32 positions (ww.h): the
+    layout is a pure permutation of App. H words, zero-padded to 32-row tiles and 4-word
+    slabs."""
+    W = (m + 15) // 16
+    S = (W + 3) // 4
+    T = (n + 31) // 32
+    out = np.zeros((T, S, 32, 4, 4), np.uint32)  # tile, slab, row, plane, word-in-slab
+    pw = np.zeros((4, T * 32, S * 4), np.uint32)
+    pw[:, :n, :W] = planar
+    pw = pw.reshape(4, T, 32, S, 4)
+    out[:] = pw.transpose(1, 3, 2, 0, 4)
+    return out.reshape(-1)
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (3, 17), (32, 64), (33, 65), (70, 300), (64, 2048)])
+def test_tile32_pack_is_app_h_words_retiled(n, m):
+    planes = wi.planes(n * 7 + m, n, m, wi.UNIFORM3)
+    got = ww.pack_ternary(planes, ww.LAYOUT_TILE32)
+    assert got.nbytes == ww.packed_bytes(n, m, ww.LAYOUT_TILE32)
+    assert got.nbytes == ((n + 31) // 32) * ((m + 63) // 64) * 2048
+    want = _tile32_from_app_h(orc.pack_planar(planes), n, m)
+    assert np.array_equal(got, want)
+    assert np.array_equal(ww.unpack_ternary(got, n, m, ww.LAYOUT_TILE32), planes)
+    for src in (ww.LAYOUT_PLANAR, ww.LAYOUT_COL4):
+        other = ww.pack_ternary(planes, src)
+        assert np.array_equal(ww.repack(other, n, m, src, ww.LAYOUT_TILE32), got)
+        assert np.array_equal(ww.repack(got, n, m, ww.LAYOUT_TILE32, src), other)
+
+
+def test_tile32_sizes_match_other_layouts_on_llama_shapes():
+    for n, m in ((2048, 2048), (5504, 2048), (2048, 5504), (6144, 2048), (11008, 2048)):
+        assert ww.packed_bytes(n, m, ww.LAYOUT_TILE32) == ww.packed_bytes(n, m) == n * m
+    assert ww._lib.ww_packed_bytes_layout(4, 4, 9) == 0
+
+
+def _tcv_maxc(n, m, sms=148):
+    T, S = (n + 31) // 32, (m + 63) // 64
+    U = T * S
+    G = min(U, sms)
+    own = lambda u: ((u + 1) * G - 1) // U  # noqa: E731
+    return T, max([1] + [own((t + 1) * S - 1) - own(t * S) for t in range(T)])
+
+
+def test_tcv_workspace_bytes():
+    """T tiles x (most contributing CTAs of a split tile) x 128 M-rows x NB flagged 8-byte
+    words; the planner assumes the device's SM count (148 without a GPU)."""
+    for (n, m, B) in ((2048, 5504, 1), (2048, 2048, 2), (11008, 2048, 1), (33, 10, 3)):
+        T, maxc = _tcv_maxc(n, m)
+        NB = 16 if B <= 2 else 32
+        assert ww.tcv_workspace_bytes(n, m, B) == T * maxc * 128 * NB * 8
+    assert ww.tcv_workspace_bytes(10, 10, 5) == 0 and ww.tcv_workspace_bytes(0, 10, 1) == 0
