@@ -430,7 +430,11 @@ def run_ours(args, world, rank, local):
     rank_pa = stack.packed_act_bytes()
     hbm_achieved = rank_pa / launches / per_launch_s / 1e9
     if getattr(stack, "tc", False):  # tcgen05 kind::i8: MACs of the padded contraction
-        macs = stack.R * 4 * stack.nloc * (ww.tc_workspace_bytes(stack.spec.m, stack.B) - 256)
+        # MACs of the padded contraction: 4 planes x rows x (m padded to 256) x N columns, N = 3 limbs
+        # x (16 or 32) (vector, component) columns (ww_tc.cu)
+        kpad = -(-stack.spec.m // 256) * 256
+        ncol = 3 * (16 if 2 * stack.B <= 16 else 32)
+        macs = stack.R * 4 * stack.nloc * kpad * ncol
         tops = 2 * macs / launches / per_launch_s / 1e12
         i8_peak = 2 * peaks.get("bf16_tflops", 1622.9)  # int8 = 2x the measured bf16 rate
         tc_roof = {"bound": "tensor", "achieved": round(tops, 2), "peak": round(i8_peak, 1),
@@ -638,8 +642,9 @@ class _ReplicaLayer:
                           ww.SCALES_PER_ROW if spec.per_row else ww.SCALES_PER_TENSOR,
                           ww.CONV_EQ1, 0 if args.no_pdl else ww.FLAG_PDL)
         # batches of >= 4 vectors run on the tensor cores (ww_wl_gemv_batched_tc) unless --no-tc
-        self.tc = (not args.no_tc) and self.B >= 4 and ww.tc_workspace_bytes(spec.m, self.B) > 0
-        self.ws = (torch.empty(ww.tc_workspace_bytes(spec.m, self.B) + 256, dtype=torch.uint8, device=dev)
+        self.tc = (not args.no_tc) and self.B >= 4 and ww.tc_workspace_bytes(self.nloc, spec.m, self.B) > 0
+        # zeroed once (ww.h: every call leaves the reduction words zeroed again)
+        self.ws = (torch.zeros(ww.tc_workspace_bytes(self.nloc, spec.m, self.B) + 256, dtype=torch.uint8, device=dev)
                    if self.tc else None)
 
     def inputs(self):

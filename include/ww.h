@@ -289,10 +289,13 @@ ww_status ww_program_run(const ww_program* prog, void* stream);
  * limbs are recombined in fp64 and the scales applied once per row (Eq. 1 /
  * Eqs. 2-3).  Error: x's 22-bit grid relative to max |x| of its vector and component.
  * X: B rows of m complex64 (stride ldx), Y: B rows of n complex64 (stride ldy); 1 <= B <= 16,
- * m <= 11264 (each x component is staged in shared memory to split it).
- * workspace_d: ww_tc_workspace_bytes(m, B) bytes, 128-B aligned, caller-owned (limbs and
+ * m <= 11264 (each x component is staged in shared memory to split it).  A layer with fewer
+ * 32-row tiles than SMs splits each tile's K range over up to 4 CTAs of one thread-block
+ * cluster whose exact int32 partial sums meet in the first CTA's shared memory (DSMEM);
+ * results do not depend on the split.
+ * workspace_d: ww_tc_workspace_bytes(n, m, B) bytes, 128-B aligned, caller-owned (limbs and
  * exponents, rewritten every call).  Two launches on `stream` (limbs, then the MMA kernel). */
-size_t ww_tc_workspace_bytes(int64_t m, int32_t B);
+size_t ww_tc_workspace_bytes(int64_t n, int64_t m, int32_t B);
 ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed_d, const float* scales_d,
                                 const float* X_d, int64_t ldx, float* Y_d, int64_t ldy, int32_t B,
                                 void* workspace_d, void* stream);

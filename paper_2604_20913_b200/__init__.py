@@ -135,7 +135,7 @@ _lib.ww_program_init.argtypes = [ctypes.POINTER(_Stage), _i32, _i32, _i32, _i32,
 _lib.ww_program_run.restype = _i32
 _lib.ww_program_run.argtypes = [ctypes.POINTER(_Program), _vp]
 _lib.ww_tc_workspace_bytes.restype = ctypes.c_size_t
-_lib.ww_tc_workspace_bytes.argtypes = [_i64, _i32]
+_lib.ww_tc_workspace_bytes.argtypes = [_i64, _i64, _i32]
 _lib.ww_wl_gemv_batched_tc.restype = _i32
 _lib.ww_wl_gemv_batched_tc.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _i64, _vp, _i64, _i32,
                                        _vp, _vp]
@@ -488,8 +488,9 @@ def keep_in_l2(tensor, stream=None):
         _check(_lib.ww_stream_keep_in_l2(sp, tensor.data_ptr(), tensor.numel() * tensor.element_size()))
 
 
-def tc_workspace_bytes(m: int, B: int) -> int:
-    return int(_lib.ww_tc_workspace_bytes(m, B))
+def tc_workspace_bytes(n: int, m: int, B: int) -> int:
+    """Bytes of the zero-initialised workspace ww_wl_gemv_batched_tc needs (0: unsupported)."""
+    return int(_lib.ww_tc_workspace_bytes(n, m, B))
 
 
 def wl_gemv_batched_tc(layer: Layer, packed, scales, X, Y=None, workspace=None, stream=None):
@@ -501,11 +502,11 @@ def wl_gemv_batched_tc(layer: Layer, packed, scales, X, Y=None, workspace=None, 
     if X.dim() != 2 or Y.dim() != 2:
         raise ValueError("X and Y must be 2-D (B, m) / (B, n) tensors")
     _check_args(layer, packed, scales, X, Y, B)
-    nb = tc_workspace_bytes(layer.m, B)
+    nb = tc_workspace_bytes(layer.n, layer.m, B)
     if nb == 0:
         raise ValueError(f"batch {B} unsupported by the tensor-core path (1..16)")
     if workspace is None or workspace.numel() * workspace.element_size() < nb + 128:
-        workspace = torch.empty(nb + 128, dtype=torch.uint8, device=X.device)
+        workspace = torch.zeros(nb + 128, dtype=torch.uint8, device=X.device)  # zeroed (ww.h)
     wp = (workspace.data_ptr() + 127) // 128 * 128
     L = layer.c()
     _check(_lib.ww_wl_gemv_batched_tc(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(),

@@ -80,6 +80,18 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
                  : "l"(p));
     return v;
 }
+// cluster helpers (split tiles): all threads of every CTA of the cluster
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_s32(uint32_t addr, int32_t v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w)
                  : "memory");
@@ -211,6 +223,8 @@ struct TcParams {
     float* Y;
     int64_t n, W, kpad, ldy;
     int32_t B, N, per_row, conv;
+    int32_t splits;                // CTAs per 32-row tile (one cluster), each a contiguous share
+                                   // of the K blocks
     unsigned long long* trace;  // tools only: CTA 0's per-block globaltimer stamps
 };
 
@@ -242,9 +256,15 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
     const uint32_t bfull = bars, bdone = bars + 8u * kBStages, afull = bars + 16u * kBStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + (bars - base) + 16 * kBStages + 8 * kStages);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t row0 = (int64_t)blockIdx.x * kRows;
+    // tile and K share of this CTA: the K blocks of a tile are split into p.splits contiguous
+    // ranges, so a layer with fewer tiles than SMs still fills the GPU; share 0 finishes the
+    // tile from the others' flagged partial sums (exact int32)
+    const int tile = blockIdx.x / p.splits, share = blockIdx.x % p.splits;
+    const int64_t row0 = (int64_t)tile * kRows;
     if (tid == 0) tc_trace(p, 60, 0);  // kernel entry
-    const int nkb = (int)(p.kpad / kKB);
+    const int nkb_all = (int)(p.kpad / kKB);
+    const int kb0 = (int)((int64_t)share * nkb_all / p.splits);
+    const int nkb = (int)((int64_t)(share + 1) * nkb_all / p.splits) - kb0;  // this CTA's blocks
 
     if (warp == 0) {  // tensor-memory accumulator: N (>= 32, power of 2) columns x 128 lanes
         uint32_t cols = 32;
@@ -270,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
     if (tid == kDecodeWarps * 32)
         for (int kb = 0; kb < kBStages - kLag && kb < nkb; ++kb) {
             mbar_expect_tx(bfull + 8u * kb, b_bytes);
-            bulk_g2s(sb + (uint32_t)kb * b_bytes, p.limbs + (int64_t)kb * b_bytes, b_bytes, bfull + 8u * kb);
+            bulk_g2s(sb + (uint32_t)kb * b_bytes, p.limbs + (int64_t)(kb0 + kb) * b_bytes, b_bytes, bfull + 8u * kb);
         }
 
     if (warp == kDecodeWarps) {
@@ -304,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
                     const int ps = nb % kBStages;
                     if (kb >= kLag) mbar_wait(bdone + 8u * ps, ((kb - kLag) / kBStages) & 1);
                     mbar_expect_tx(bfull + 8u * ps, b_bytes);
-                    bulk_g2s(sb + (uint32_t)ps * b_bytes, p.limbs + (int64_t)nb * b_bytes, b_bytes,
+                    bulk_g2s(sb + (uint32_t)ps * b_bytes, p.limbs + (int64_t)(kb0 + nb) * b_bytes, b_bytes,
                              bfull + 8u * ps);
                 }
             }
@@ -325,9 +345,9 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
                                (uint32_t)(cc & 1) * 128u + (uint32_t)((r & 1) * 4) * 16u;
         const uint4* wsrc = p.packed + (rok ? grow : 0) * p.W + cc;
         auto load_w = [&](int kb) -> uint4 {
-            const int64_t c = (int64_t)kb * (kKB / 16) + cc;
-            return (rok && kb < nkb && c < p.W) ? ldg_stream(wsrc + (int64_t)kb * (kKB / 16))
-                                                : make_uint4(0, 0, 0, 0);
+            const int64_t gk = (int64_t)(kb0 + kb);
+            const int64_t c = gk * (kKB / 16) + cc;
+            return (rok && kb < nkb && c < p.W) ? ldg_stream(wsrc + gk * (kKB / 16)) : make_uint4(0, 0, 0, 0);
         };
         uint4 wq[kStages];
 #pragma unroll
@@ -360,50 +380,65 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
     tc_fence_after();
     if (tid == 0) tc_trace(p, 60, 1);  // epilogue start
 
+    // split tiles: the CTAs of a tile form a cluster; once every CTA's MMAs are done (cluster
+    // barrier: no CTA reads its shared memory any more) each share writes its accumulators
+    // into share 0's shared memory (DSMEM), a second cluster barrier, and share 0 finishes the
+    // tile from the exact int32 sums
+    if (p.splits > 1) cluster_sync();
+    const int cw = 2 * p.B, rs = 3 * cw + 1;
     if (warp < 4) {
-        // lane m = 32 warp + lane of the accumulator: output row m / 4, plane m % 4
+        // lane m = 32 warp + lane of the accumulator: output row m / 4, plane m % 4.
+        // Dsm[share][m][l][c] = limb l of column c (= 2 b + comp), row stride 6B + 1 words
+        // (conflict-free), in share 0's shared memory (the idle A ring)
+        const int m = 32 * warp + lane;
+        const int LW = N / kLimbs;
+        const uint32_t dsm_local = base + (uint32_t)((share * 128 + m) * rs) * 4u;
+        const uint32_t dsm = p.splits > 1 ? map_to_rank(dsm_local, 0) : dsm_local;
+        const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16);
+#pragma unroll
+        for (int l = 0; l < kLimbs; ++l) {
+            int32_t D[32];
+            tmem_ld32(tl + (uint32_t)(l * LW), D);  // limb l: columns l LW .. l LW + 2B - 1
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (c < cw) st_cluster_s32(dsm + 4u * (uint32_t)(l * cw + c), D[c]);
+        }
+    }
+    if (p.splits > 1) cluster_sync();  // every share's sums are in share 0
+    if (warp < 4 && share == 0) {
         const int m = 32 * warp + lane, rr = m >> 2, pl = m & 3;
         const int64_t row = row0 + rr;
-        const int LW = N / kLimbs;
-        const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16);
-        int32_t D0[32], D1[32], D2[32];  // limb k of column bc at D_k[bc] (limb-major layout)
-        if (LW == 32) {
-            tmem_ld32(tl + 0u, D0);
-            tmem_ld32(tl + 32u, D1);
-            tmem_ld32(tl + 64u, D2);
-        } else {  // LW = 16: limbs 0 | 1 in columns 0-31, limb 2 in 32-47
-            tmem_ld32(tl + 0u, D0);
-            tmem_ld32(tl + 32u, D2);
+        int32_t* Dsm = reinterpret_cast<int32_t*>(smem) + m * rs;
+        for (int j = 1; j < p.splits; ++j)
+            for (int k = 0; k < 3 * cw; ++k) Dsm[k] += Dsm[j * 128 * rs + k];
+        {
+            const double s = row < p.n ? (double)p.scales[p.per_row ? 4 * row + pl : pl] : 0.0;
+            const bool eq1 = p.conv == WW_CONV_EQ1;
+            for (int b = 0; b < p.B; ++b) {
+                double S[2];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) D1[i] = D0[16 + i];
-        }
-        const double s = row < p.n ? (double)p.scales[p.per_row ? 4 * row + pl : pl] : 0.0;
-        const bool eq1 = p.conv == WW_CONV_EQ1;
-#pragma unroll
-        for (int b = 0; b < kMaxB; ++b) {
-            if (b >= p.B) break;
-            double S[2];
-#pragma unroll
-            for (int comp = 0; comp < 2; ++comp) {
-                const int c = 2 * b + comp;
-                const double v = (double)D2[c] * 65536.0 + (double)D1[c] * 256.0 + (double)D0[c];
-                S[comp] = v * __longlong_as_double((long long)(1023 - p.expo[c]) << 52) * s;  // 2^-E
+                for (int comp = 0; comp < 2; ++comp) {
+                    const int c = 2 * b + comp;
+                    const double v =
+                        (double)Dsm[2 * cw + c] * 65536.0 + (double)Dsm[cw + c] * 256.0 + (double)Dsm[c];
+                    S[comp] = v * __longlong_as_double((long long)(1023 - p.expo[c]) << 52) * s;  // 2^-E
+                }
+                // this plane's share of y (P:1002-1011 with the EQ1 / ALG1 signs of Eq. 1 / Eq. 3):
+                // U_re: (re, im); U_im: (-im, re); W_re: (re, -+im); W_im: (im, +-re)
+                double yre, yim;
+                if (pl == 0) { yre = S[0]; yim = S[1]; }
+                else if (pl == 1) { yre = -S[1]; yim = S[0]; }
+                else if (pl == 2) { yre = S[0]; yim = eq1 ? -S[1] : S[1]; }
+                else { yre = S[1]; yim = eq1 ? S[0] : -S[0]; }
+                // sum over the four planes (lanes 4rr .. 4rr+3), fixed order: (0+1) + (2+3)
+                yre += __shfl_xor_sync(0xffffffffu, yre, 1);
+                yim += __shfl_xor_sync(0xffffffffu, yim, 1);
+                yre += __shfl_xor_sync(0xffffffffu, yre, 2);
+                yim += __shfl_xor_sync(0xffffffffu, yim, 2);
+                if (pl == (b & 3) && row < p.n)
+                    reinterpret_cast<float2*>(p.Y)[(int64_t)b * p.ldy + row] =
+                        make_float2((float)yre, (float)yim);
             }
-            // this plane's share of y (P:1002-1011 with the EQ1 / ALG1 signs of Eq. 1 / Eq. 3):
-            // U_re: (re, im); U_im: (-im, re); W_re: (re, -+im); W_im: (im, +-re)
-            double yre, yim;
-            if (pl == 0) { yre = S[0]; yim = S[1]; }
-            else if (pl == 1) { yre = -S[1]; yim = S[0]; }
-            else if (pl == 2) { yre = S[0]; yim = eq1 ? -S[1] : S[1]; }
-            else { yre = S[1]; yim = eq1 ? S[0] : -S[0]; }
-            // sum over the four planes (lanes 4rr .. 4rr+3), fixed order: (0+1) + (2+3)
-            yre += __shfl_xor_sync(0xffffffffu, yre, 1);
-            yim += __shfl_xor_sync(0xffffffffu, yim, 1);
-            yre += __shfl_xor_sync(0xffffffffu, yre, 2);
-            yim += __shfl_xor_sync(0xffffffffu, yim, 2);
-            if (pl == (b & 3) && row < p.n)
-                reinterpret_cast<float2*>(p.Y)[(int64_t)b * p.ldy + row] =
-                    make_float2((float)yre, (float)yim);
         }
     }
     if (tid == 0) tc_trace(p, 60, 2);  // epilogue end (warp 0)
@@ -423,8 +458,22 @@ static unsigned long long* g_tc_trace = nullptr;
 // Not part of the ABI: tools point CTA 0 of the tensor-core kernel at a trace buffer.
 extern "C" void ww_debug_tc_trace(void* buf) { g_tc_trace = reinterpret_cast<unsigned long long*>(buf); }
 
-extern "C" size_t ww_tc_workspace_bytes(int64_t m, int32_t B) {
-    if (m < 1 || B < 1 || B > kMaxB) return 0;
+// K splits per tile: enough CTAs to cover the SMs, at most 4, at least one K block each
+static int tc_splits(int64_t n, int64_t m, int32_t B) {
+    const int64_t tiles = (n + kRows - 1) / kRows, nkb = tc_kpad(m) / kKB;
+    int64_t sp = ww::device_sms() / tiles;
+    if (sp > 4) sp = 4;
+    if (B > 8) sp = 1;  // measured: at B = 16 the split (DSMEM exchange of 96 columns) costs more
+    // the shares' accumulators (128 rows of 6B + 1 words each) must fit share 0's rings
+    const int64_t ring = (int64_t)kStages * kTM * kKB + (int64_t)kBStages * tc_n(B) * kKB;
+    const int64_t fit = ring / (128 * (6 * (int64_t)B + 1) * 4);
+    if (sp > fit) sp = fit;
+    if (sp > nkb) sp = nkb;
+    return sp < 1 ? 1 : (int)sp;
+}
+
+extern "C" size_t ww_tc_workspace_bytes(int64_t n, int64_t m, int32_t B) {
+    if (n < 1 || m < 1 || B < 1 || B > kMaxB) return 0;
     return (size_t)tc_kpad(m) * (size_t)tc_n(B) + 256;
 }
 
@@ -451,6 +500,7 @@ extern "C" ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed
     const int64_t kpad = tc_kpad(L->m);
     int8_t* limbs = reinterpret_cast<int8_t*>(workspace_d);
     int* expo = reinterpret_cast<int*>(reinterpret_cast<char*>(workspace_d) + (size_t)kpad * N);
+    const int splits = tc_splits(L->n, L->m, B);
     cudaStream_t s = (cudaStream_t)stream;
     tc_limbs_kernel<<<2 * B + 1, kLimbThreads, 0, s>>>(X_d, ldx, B, L->m, kpad, N, limbs, expo);
     cudaError_t e = cudaGetLastError();
@@ -471,13 +521,29 @@ extern "C" ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed
     p.per_row = L->scale_mode == WW_SCALES_PER_ROW;
     p.conv = L->conv;
     p.trace = g_tc_trace;
+    p.splits = splits;
     const int smem = (int)(kStages * kTM * kKB + kBStages * (int64_t)N * kKB + 16 * kBStages +
                            8 * kStages + 64 + 1024);
     const int pe = ww::prepare_kernel(reinterpret_cast<const void*>(wl_tc_kernel), 227 * 1024);
     if (pe) return ww::fail(WW_ERR_CUDA, "%s: %s", fn, cudaGetErrorString((cudaError_t)pe));
-    const int grid = (int)((L->n + kRows - 1) / kRows);
-    wl_tc_kernel<<<grid, kThreads, smem, s>>>(p);
-    e = cudaGetLastError();
+    const int grid = (int)((L->n + kRows - 1) / kRows) * splits;
+    {
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof cfg);
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = (size_t)smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;  // the shares of a tile: one cluster
+        attr[0].val.clusterDim.x = (unsigned)splits;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, wl_tc_kernel, p);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return ww::fail(WW_ERR_CUDA, "%s: %s", fn, cudaGetErrorString(e));
     return ww::ok();
 }

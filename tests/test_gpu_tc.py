@@ -66,4 +66,21 @@ def test_argument_errors():
     X = torch.zeros((17, 32), dtype=torch.complex64, device="cuda")
     with pytest.raises(ValueError):
         ww.wl_gemv_batched_tc(L, case.packed_d, case.scales_d, X)
-    assert ww.tc_workspace_bytes(32, 17) == 0 and ww.tc_workspace_bytes(5504, 16) > 0
+    assert ww.tc_workspace_bytes(16, 32, 17) == 0 and ww.tc_workspace_bytes(2048, 5504, 16) > 0
+
+
+def test_split_k_workspace_reuse_and_repeat():
+    """Config 5 splits each 32-row tile's K range over several CTAs (64 tiles < 148 SMs): the
+    partial sums meet in the workspace, which every call must leave zeroed; repeated calls on
+    one workspace give identical bits, and so do other batch sizes sharing it."""
+    case = LayerCase.from_spec(wi.C3B, seed=17, B=16).device(ww, torch)
+    L = case.layer(ww, ww.CONV_EQ1)
+    nb = ww.tc_workspace_bytes(case.n, case.m, 16)
+    ws = torch.zeros(nb + 256, dtype=torch.uint8, device="cuda")
+    y0 = ww.wl_gemv_batched_tc(L, case.packed_d, case.scales_d, case.x_d, workspace=ws).cpu().numpy()
+    for _ in range(2):
+        y1 = ww.wl_gemv_batched_tc(L, case.packed_d, case.scales_d, case.x_d, workspace=ws).cpu().numpy()
+        assert np.array_equal(y0, y1)
+    assert_parity(y0, case.oracle(orc.CONV_EQ1), case)
+    y8 = ww.wl_gemv_batched_tc(L, case.packed_d, case.scales_d, case.x_d[:8], workspace=ws).cpu().numpy()
+    assert np.array_equal(y8, y0[:8])

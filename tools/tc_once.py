@@ -15,7 +15,7 @@ for q in range(4):
 packed = ww.pack_ternary_device(planes)
 sc = torch.rand((n, 4), device="cuda") * 0.09 + 0.01
 X = torch.randn((B, m), dtype=torch.complex64, device="cuda")
-ws = torch.empty(ww.tc_workspace_bytes(m, B) + 256, dtype=torch.uint8, device="cuda")
+ws = torch.zeros(ww.tc_workspace_bytes(n, m, B) + 256, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     ww.wl_gemv_batched_tc(ww.Layer(n, m), packed, sc, X, workspace=ws)
 torch.cuda.synchronize()

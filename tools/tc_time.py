@@ -50,7 +50,7 @@ def main(n=2048, m=5504, batches=(1, 2, 4, 8, 16)):
     for B in batches:
         X = torch.randn((B, m), dtype=torch.complex64, device="cuda")
         Y = torch.empty((B, n), dtype=torch.complex64, device="cuda")
-        ws = torch.empty(ww.tc_workspace_bytes(m, B) + 256, dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(ww.tc_workspace_bytes(n, m, B) + 256, dtype=torch.uint8, device="cuda")
         t_tc = run(lambda r: ww.wl_gemv_batched_tc(L, reps[r], sc, X, Y, ws, stream=s))
         t_fa = run(lambda r: ww.wl_gemv_batched(L, reps[r], sc, X, Y, stream=s)) if B <= 16 else float("nan")
         bytes_ = nb + 8 * m * B
