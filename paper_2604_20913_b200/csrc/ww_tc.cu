@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
     const uint32_t bars = sb + kBStages * b_bytes;
     const uint32_t bfull = bars, bdone = bars + 8u * kBStages, afull = bars + 16u * kBStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + (bars - base) + 16 * kBStages + 8 * kStages);
+    int* expo_s = reinterpret_cast<int*>(tmem_slot) + 4;  // the 2B exponents, staged once
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // tile and K share of this CTA: the K blocks of a tile are split into p.splits contiguous
     // ranges, so a layer with fewer tiles than SMs still fills the GPU; share 0 finishes the
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    if (tid >= 64 && tid < 64 + 2 * p.B) expo_s[tid - 64] = p.expo[tid - 64];  // read in the epilogue
     if (tid == 32) {
         for (int i = 0; i < 2 * kBStages; ++i) mbar_init(bars + 8u * i, 1);
         for (int i = 0; i < kStages; ++i) mbar_init(afull + 8u * i, kDecodeWarps);
@@ -385,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
     // into share 0's shared memory (DSMEM), a second cluster barrier, and share 0 finishes the
     // tile from the exact int32 sums
     if (p.splits > 1) cluster_sync();
+    if (tid == 0) tc_trace(p, 61, 0);
     const int cw = 2 * p.B, rs = 3 * cw + 1;
     if (warp < 4) {
         // lane m = 32 warp + lane of the accumulator: output row m / 4, plane m % 4.
@@ -404,13 +407,16 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
                 if (c < cw) st_cluster_s32(dsm + 4u * (uint32_t)(l * cw + c), D[c]);
         }
     }
+    if (tid == 0) tc_trace(p, 61, 1);
     if (p.splits > 1) cluster_sync();  // every share's sums are in share 0
+    if (tid == 0) tc_trace(p, 61, 2);
     if (warp < 4 && share == 0) {
         const int m = 32 * warp + lane, rr = m >> 2, pl = m & 3;
         const int64_t row = row0 + rr;
         int32_t* Dsm = reinterpret_cast<int32_t*>(smem) + m * rs;
         for (int j = 1; j < p.splits; ++j)
             for (int k = 0; k < 3 * cw; ++k) Dsm[k] += Dsm[j * 128 * rs + k];
+        if (tid == 0) tc_trace(p, 61, 3);
         {
             const double s = row < p.n ? (double)p.scales[p.per_row ? 4 * row + pl : pl] : 0.0;
             const bool eq1 = p.conv == WW_CONV_EQ1;
@@ -421,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
                     const int c = 2 * b + comp;
                     const double v =
                         (double)Dsm[2 * cw + c] * 65536.0 + (double)Dsm[cw + c] * 256.0 + (double)Dsm[c];
-                    S[comp] = v * __longlong_as_double((long long)(1023 - p.expo[c]) << 52) * s;  // 2^-E
+                    S[comp] = v * __longlong_as_double((long long)(1023 - expo_s[c]) << 52) * s;  // 2^-E
                 }
                 // this plane's share of y (P:1002-1011 with the EQ1 / ALG1 signs of Eq. 1 / Eq. 3):
                 // U_re: (re, im); U_im: (-im, re); W_re: (re, -+im); W_im: (im, +-re)
@@ -523,7 +529,7 @@ extern "C" ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed
     p.trace = g_tc_trace;
     p.splits = splits;
     const int smem = (int)(kStages * kTM * kKB + kBStages * (int64_t)N * kKB + 16 * kBStages +
-                           8 * kStages + 64 + 1024);
+                           8 * kStages + 64 + 4 * 2 * kMaxB + 1024);
     const int pe = ww::prepare_kernel(reinterpret_cast<const void*>(wl_tc_kernel), 227 * 1024);
     if (pe) return ww::fail(WW_ERR_CUDA, "%s: %s", fn, cudaGetErrorString((cudaError_t)pe));
     const int grid = (int)((L->n + kRows - 1) / kRows) * splits;
