@@ -478,7 +478,9 @@ def run_ours(args, world, rank, local):
         "pct_of_hbm_peak": round(100 * (pa_bytes / (ms_step * 1e-3) / 1e9) / world
                                  / peaks.get("hbm_gbs", 6650.0), 2),
         "hbm_frac": roof["hbm"]["frac"],
-        "alu_frac": roof["frac"],
+        # the FP32-add ALU fraction describes the CUDA-core kernel; on the tensor-core path
+        # the adds run in the MMAs (roofline = the int8 tensor rate)
+        "alu_frac": None if getattr(stack, "tc", False) else roof["frac"],
         "roofline": tc_roof if getattr(stack, "tc", False) else roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -577,6 +579,11 @@ def _launch_configs(ww, stack, args):
             shapes.setdefault(f"{st.name} {st.ylocal}x{st.m}", (st.ylocal, st.m))
     else:
         shapes = {f"{stack.spec.name} {stack.nloc}x{stack.spec.m}": (stack.nloc, stack.spec.m)}
+    if getattr(stack, "tc", False):
+        return {k: {"kernels": "tc_limbs_kernel (2B+1 CTAs x 1024 threads) + wl_tc_kernel (544 threads, "
+                               "one CTA per 32-row tile; the K range split over a thread-block cluster of "
+                               "up to 4 CTAs when tiles < SMs and B <= 8)",
+                    "tiles": -(-n // 32)} for k, (n, m) in shapes.items()}
     return {k: ww.query_launch(ww.Layer(max(n, 1), m), args.batch) for k, (n, m) in shapes.items()}
 
 
@@ -663,7 +670,8 @@ class _ReplicaLayer:
                 n = self.Y[0].numel() // self.world
                 dist.all_gather_into_tensor(self.Y[0], self.Y[0][self.rank * n:(self.rank + 1) * n],
                                             group=self.group)
-        return self.R * self.ww.launches_for_batch(self.B)
+        # the tensor-core path is two launches per layer (x limbs, then the MMA kernel)
+        return self.R * (2 if self.tc else self.ww.launches_for_batch(self.B))
 
     def algorithmic_bytes(self):
         m, n, B = self.spec.m, self.nloc, self.B
