@@ -536,9 +536,14 @@ def _ncu_traffic():
 
 def _e2e(stack, args, s, dev, graph, world, alg_bytes):
     """Same metric with host<->device copies in the timed region: pinned host activations
-    -> HBM each step, the last projection's gathered output -> host each step."""
+    -> HBM each step, the last projection's gathered output -> host each step.  With a CUDA
+    graph over a stack whose launches read stack.X, the inputs are double-buffered: a second
+    graph reads the second buffer, and step k's host->device copy runs on a copy stream while
+    step k-1 computes (every step still copies its own inputs inside the timed region)."""
     import torch
     import torch.distributed as dist
+    import paper_2604_20913_b200 as ww
+    from paper_2604_20913_b200.stack import WLStack
     xflat = stack.inputs().view(-1)
     xh = torch.empty(xflat.numel(), dtype=torch.complex64).pin_memory()
     xh.copy_(xflat.cpu())
@@ -547,20 +552,63 @@ def _e2e(stack, args, s, dev, graph, world, alg_bytes):
     steps = max(2, args.steps)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    pipelined = graph is not None and isinstance(stack, WLStack)
+    if pipelined:
+        # both input buffers in one allocation, so one L2 access-policy window (and one
+        # persisting carve-out) covers the two graphs' activations
+        XA = stack.X
+        Xpair = torch.empty((2, XA.numel()), dtype=XA.dtype, device=dev)
+        Xpair[0].copy_(XA)
+        Xpair[1].copy_(XA)
+        gs = []
+        try:
+            if args.x_l2_persist:
+                ww.keep_in_l2(Xpair, s)
+            for h in range(2):
+                stack.X = Xpair[h]
+                with torch.cuda.stream(s):
+                    stack.step(s)
+                torch.cuda.synchronize(dev)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    stack.step(s)
+                gs.append(g)
+        finally:
+            stack.X = XA
+        xins = [Xpair[h].view(-1)[:xflat.numel()] for h in range(2)]  # the same slice of either
+        graphs = gs
+        cs = torch.cuda.Stream(dev)
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        consumed = [torch.cuda.Event(), torch.cuda.Event()]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     with torch.cuda.stream(s):
         e0.record(s)
-        for _ in range(steps):
-            xflat.copy_(xh, non_blocking=True)
-            if graph is not None:
-                graph.replay()
+        if pipelined:
+            cs.wait_event(e0)
+        for k in range(steps):
+            if pipelined:
+                i = k & 1
+                with torch.cuda.stream(cs):
+                    if k >= 2:
+                        cs.wait_event(consumed[i])  # step k-2 has finished reading this buffer
+                    xins[i].copy_(xh, non_blocking=True)
+                    copied[i].record(cs)
+                s.wait_event(copied[i])
+                graphs[i].replay()
+                consumed[i].record(s)
             else:
-                stack.step(s)
+                xflat.copy_(xh, non_blocking=True)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    stack.step(s)
             yh.copy_(last, non_blocking=True)
         e1.record(s)
     torch.cuda.synchronize(dev)
+    if pipelined and args.x_l2_persist:
+        ww.keep_in_l2(stack.inputs(), s)
     ms = e0.elapsed_time(e1) / steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -568,7 +616,9 @@ def _e2e(stack, args, s, dev, graph, world, alg_bytes):
     ms = float(t.item())
     return {"value": round(alg_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8),
-            "ms_per_step": round(ms, 4)}
+            "ms_per_step": round(ms, 4),
+            "overlap": ("inputs double-buffered: step k's host->device copy on a copy stream "
+                        "during step k-1" if pipelined else "serial copies on the compute stream")}
 
 
 def _launch_configs(ww, stack, args):
