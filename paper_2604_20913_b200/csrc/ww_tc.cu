@@ -408,19 +408,31 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
         }
     }
     if (tid == 0) tc_trace(p, 61, 1);
-    if (p.splits > 1) cluster_sync();  // every share's sums are in share 0
+    // every share's sums are in share 0 (and visible to all of its warps, which finish the tile)
+    if (p.splits > 1) cluster_sync();
+    else __syncthreads();
     if (tid == 0) tc_trace(p, 61, 2);
-    if (warp < 4 && share == 0) {
-        const int m = 32 * warp + lane, rr = m >> 2, pl = m & 3;
+    if (warp < kDecodeWarps && share == 0) {
+        // the 16 decode warps finish the tile: warp group grp = warp / 4 takes the vectors
+        // b = grp, grp + 4, ... (summing their columns over the shares first); warp % 4 picks
+        // the M-rows as in the accumulator (lane quarter)
+        const int q = warp & 3, grp = warp >> 2;
+        const int m = 32 * q + lane, rr = m >> 2, pl = m & 3;
         const int64_t row = row0 + rr;
         int32_t* Dsm = reinterpret_cast<int32_t*>(smem) + m * rs;
-        for (int j = 1; j < p.splits; ++j)
-            for (int k = 0; k < 3 * cw; ++k) Dsm[k] += Dsm[j * 128 * rs + k];
         if (tid == 0) tc_trace(p, 61, 3);
         {
             const double s = row < p.n ? (double)p.scales[p.per_row ? 4 * row + pl : pl] : 0.0;
             const bool eq1 = p.conv == WW_CONV_EQ1;
-            for (int b = 0; b < p.B; ++b) {
+            for (int b = grp; b < p.B; b += 4) {
+                for (int j = 1; j < p.splits; ++j)
+#pragma unroll
+                    for (int l = 0; l < kLimbs; ++l)
+#pragma unroll
+                        for (int comp = 0; comp < 2; ++comp) {
+                            const int k = l * cw + 2 * b + comp;
+                            Dsm[k] += Dsm[j * 128 * rs + k];
+                        }
                 double S[2];
 #pragma unroll
                 for (int comp = 0; comp < 2; ++comp) {
