@@ -19,6 +19,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "ww.h"
@@ -89,8 +90,9 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
-__device__ __forceinline__ void st_cluster_s32(uint32_t addr, int32_t v) {
-    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, int32_t a, int32_t b, int32_t c, int32_t d) {
+    asm volatile("st.shared::cluster.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
 }
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w)
@@ -229,7 +231,7 @@ struct TcParams {
 };
 
 __device__ __forceinline__ void tc_trace(const TcParams& p, int kb, int ev) {
-    if (p.trace && blockIdx.x == 0) p.trace[kb * 8 + ev] = clock64();  // SM cycles
+    if (p.trace && blockIdx.x < 2) p.trace[blockIdx.x * 512 + kb * 8 + ev] = clock64();  // SM cycles (CTAs 0, 1)
 }
 
 // int8 {-1, 0, +1} of plane p for the four columns of one COL4 word (byte = column, bits
@@ -388,7 +390,9 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
     // tile from the exact int32 sums
     if (p.splits > 1) cluster_sync();
     if (tid == 0) tc_trace(p, 61, 0);
-    const int cw = 2 * p.B, rs = 3 * cw + 1;
+    // row of a lane: 3 limbs x cwp (2B padded to 4) words + 4, 16-byte aligned for the vector
+    // stores into share 0
+    const int cw = 2 * p.B, cwp = (cw + 3) & ~3, rs = 3 * cwp + 4;
     if (warp < 4) {
         // lane m = 32 warp + lane of the accumulator: output row m / 4, plane m % 4.
         // Dsm[share][m][l][c] = limb l of column c (= 2 b + comp), row stride 6B + 1 words
@@ -403,8 +407,8 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
             int32_t D[32];
             tmem_ld32(tl + (uint32_t)(l * LW), D);  // limb l: columns l LW .. l LW + 2B - 1
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (c < cw) st_cluster_s32(dsm + 4u * (uint32_t)(l * cw + c), D[c]);
+            for (int c = 0; c < 32; c += 4)
+                if (c < cw) st_cluster_v4(dsm + 4u * (uint32_t)(l * cwp + c), D[c], D[c + 1], D[c + 2], D[c + 3]);
         }
     }
     if (tid == 0) tc_trace(p, 61, 1);
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
                     for (int l = 0; l < kLimbs; ++l)
 #pragma unroll
                         for (int comp = 0; comp < 2; ++comp) {
-                            const int k = l * cw + 2 * b + comp;
+                            const int k = l * cwp + 2 * b + comp;
                             Dsm[k] += Dsm[j * 128 * rs + k];
                         }
                 double S[2];
@@ -438,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
                 for (int comp = 0; comp < 2; ++comp) {
                     const int c = 2 * b + comp;
                     const double v =
-                        (double)Dsm[2 * cw + c] * 65536.0 + (double)Dsm[cw + c] * 256.0 + (double)Dsm[c];
+                        (double)Dsm[2 * cwp + c] * 65536.0 + (double)Dsm[cwp + c] * 256.0 + (double)Dsm[c];
                     S[comp] = v * __longlong_as_double((long long)(1023 - expo_s[c]) << 52) * s;  // 2^-E
                 }
                 // this plane's share of y (P:1002-1011 with the EQ1 / ALG1 signs of Eq. 1 / Eq. 3):
@@ -481,10 +485,9 @@ static int tc_splits(int64_t n, int64_t m, int32_t B) {
     const int64_t tiles = (n + kRows - 1) / kRows, nkb = tc_kpad(m) / kKB;
     int64_t sp = ww::device_sms() / tiles;
     if (sp > 4) sp = 4;
-    if (B > 8) sp = 1;  // measured: at B = 16 the split (DSMEM exchange of 96 columns) costs more
     // the shares' accumulators (128 rows of 6B + 1 words each) must fit share 0's rings
     const int64_t ring = (int64_t)kStages * kTM * kKB + (int64_t)kBStages * tc_n(B) * kKB;
-    const int64_t fit = ring / (128 * (6 * (int64_t)B + 1) * 4);
+    const int64_t fit = ring / (128 * (3 * ((2 * (int64_t)B + 3) & ~3) + 4) * 4);
     if (sp > fit) sp = fit;
     if (sp > nkb) sp = nkb;
     return sp < 1 ? 1 : (int)sp;

@@ -7,7 +7,7 @@ sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import paper_2604_20913_b200 as ww, ww_inputs as wi
 from _wl import LayerCase
 case = LayerCase(300, 517, seed=3, B=8).device(ww, torch)
-buf = torch.zeros(64 * 8, dtype=torch.int64).pin_memory()
+buf = torch.zeros(2 * 64 * 8, dtype=torch.int64).pin_memory()
 ww._lib.ww_debug_tc_trace(ctypes.c_void_p(buf.data_ptr()))
 L = case.layer(ww, ww.CONV_EQ1)
 n_arg = sys.argv[1:] and sys.argv[1]
@@ -20,9 +20,12 @@ th = threading.Thread(target=lambda: (torch.cuda.synchronize(), done.append(1)),
 th.start()
 th.join(5)
 print("kernel finished:", bool(done), flush=True)
-t = buf.numpy().reshape(64, 8)
-for kb in list(range(3)) + [59, 60, 61]:
-    if t[kb].any():
-        print(kb, list(int(v) for v in t[kb]))
+T = buf.numpy().reshape(2, 64, 8)
+for c in range(2):
+    t = T[c]
+    print("CTA", c, "(clock64 is per SM: compare within a CTA only)")
+    for kb in list(range(3)) + [int(np.nonzero(t[:59].any(axis=1))[0].max())] + [60, 61]:
+        if t[kb].any():
+            print(" ", kb, list(int(v - t[60][0]) for v in t[kb] if v))
 print("done-check", flush=True)
 import os; os._exit(0)
