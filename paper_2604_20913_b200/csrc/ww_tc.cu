@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(kLimbThreads) tc_limbs_kernel(const float* __r
                                                                 int* __restrict__ expo) {
     __shared__ float xs[kLimbMaxM];
     __shared__ float red[kLimbThreads / 32];
+    // the MMA kernel (launched as a programmatic dependent) starts decoding weights now; it
+    // waits (griddepcontrol.wait) before it reads the limbs or the exponents
+    asm volatile("griddepcontrol.launch_dependents;" :::);
     const int bc = blockIdx.x, LW = N / kLimbs;
     const int64_t ng = kpad / 16;  // 16-column groups: one 16-byte core-matrix row each
     if (bc == 2 * B) {
@@ -278,7 +281,10 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    if (tid >= 64 && tid < 64 + 2 * p.B) expo_s[tid - 64] = p.expo[tid - 64];  // read in the epilogue
+    if (tid >= 64 && tid < 64 + 2 * p.B) {  // read in the epilogue; written by the limb kernel
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        expo_s[tid - 64] = p.expo[tid - 64];
+    }
     if (tid == 32) {
         for (int i = 0; i < 2 * kBStages; ++i) mbar_init(bars + 8u * i, 1);
         for (int i = 0; i < kStages; ++i) mbar_init(afull + 8u * i, kDecodeWarps);
@@ -291,6 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
     const uint32_t idesc = umma_idesc_i8(N);
     // the limbs of the first kStages - 1 blocks in flight (block kb + kStages - 1 is requested
     // once the MMAs of block kb - 1 have released its slot)
+    // the limbs come from tc_limbs_kernel, the preceding (PDL primary) launch: the MMA warp waits
+    // for it; the decode warps start on the weights at once
+    if (warp == kDecodeWarps) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == kDecodeWarps * 32)
         for (int kb = 0; kb < kBStages - kLag && kb < nkb; ++kb) {
             mbar_expect_tx(bfull + 8u * kb, b_bytes);
@@ -555,13 +564,15 @@ extern "C" ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed
         cfg.blockDim = dim3(kThreads);
         cfg.dynamicSmemBytes = (size_t)smem;
         cfg.stream = s;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;  // the shares of a tile: one cluster
         attr[0].val.clusterDim.x = (unsigned)splits;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the limb kernel
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = 2;
         e = cudaLaunchKernelEx(&cfg, wl_tc_kernel, p);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
