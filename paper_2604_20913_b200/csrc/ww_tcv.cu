@@ -726,32 +726,45 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tcv_kernel(const __grid_consta
                     for (int k = 0; k < NB; ++k)
                         if (k < cols) st_relaxed64(w + k, (1ull << 32) | (uint32_t)D[k]);
                 } else {
-                    for (int j = 0; j < (int)(c1 - c0); ++j) {
-                        unsigned long long* w = p.ws + ((t * p.maxc + j) * 128 + mr) * NB;
+                    // 8 columns x every contributor slot (at most 4 in flight per column) polled
+                    // together: every not-yet-flagged word re-polled in the same pass (one round
+                    // trip per pass); bounded: a workspace that was not zeroed fails loudly
+                    const int nj = (int)(c1 - c0);
 #pragma unroll
-                        for (int k0 = 0; k0 < NB; k0 += 8) {  // 8 words in flight at a time
-                            if (k0 < cols) {
-                            unsigned long long v[8];
+                    for (int k0 = 0; k0 < NB; k0 += 8) {
+                        if (k0 < cols) {
+                            for (int j0 = 0; j0 < nj; j0 += 4) {
+                                unsigned long long v[4][8];
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) v[k] = k0 + k < cols ? ld_relaxed64(w + k0 + k) : (1ull << 32);
-                            // every not-yet-flagged word re-polled together (one round trip per pass);
-                            // bounded: a workspace that was not zeroed fails loudly
-                            for (long long pass = 0;; ++pass) {
-                                bool all = true;
+                                for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-                                for (int k = 0; k < 8; ++k) all = all && (v[k] >> 32) != 0;
-                                if (all) break;
-                                if (pass > (1ll << 24)) __trap();
+                                    for (int k = 0; k < 8; ++k)
+                                        v[jj][k] = (j0 + jj < nj && k0 + k < cols)
+                                                       ? ld_relaxed64(p.ws + ((t * p.maxc + j0 + jj) * 128 + mr) * NB + k0 + k)
+                                                       : (1ull << 32);
+                                for (long long pass = 0;; ++pass) {
+                                    bool all = true;
 #pragma unroll
-                                for (int k = 0; k < 8; ++k)
-                                    if ((v[k] >> 32) == 0) v[k] = ld_relaxed64(w + k0 + k);
-                            }
+                                    for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-                            for (int k = 0; k < 8; ++k)
-                                if (k0 + k < cols) {
-                                    D[k0 + k] += (int32_t)(uint32_t)v[k];
-                                    w[k0 + k] = 0ull;
+                                        for (int k = 0; k < 8; ++k) all = all && (v[jj][k] >> 32) != 0;
+                                    if (all) break;
+                                    if (pass > (1ll << 24)) __trap();
+#pragma unroll
+                                    for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                                        for (int k = 0; k < 8; ++k)
+                                            if ((v[jj][k] >> 32) == 0)
+                                                v[jj][k] = ld_relaxed64(p.ws + ((t * p.maxc + j0 + jj) * 128 + mr) * NB + k0 + k);
                                 }
+#pragma unroll
+                                for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                                    for (int k = 0; k < 8; ++k)
+                                        if (j0 + jj < nj && k0 + k < cols) {
+                                            D[k0 + k] += (int32_t)(uint32_t)v[jj][k];
+                                            p.ws[((t * p.maxc + j0 + jj) * 128 + mr) * NB + k0 + k] = 0ull;
+                                        }
                             }
                         }
                     }
