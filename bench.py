@@ -681,12 +681,16 @@ class _ReplicaLayer:
         self.B = args.batch
         sh = ww.shard_plan(spec.n, spec.m, world, rank)
         self.shard, self.nloc = sh, sh.row_end - sh.row_begin
-        nb = self.nloc * ww.packed_bytes(1, spec.m)
+        # batches of >= 4 vectors run on the tensor cores (ww_wl_gemv_batched_tc, weights in
+        # WW_LAYOUT_TILE32) unless --no-tc; everything else on the CUDA-core kernel (COL4)
+        self.tc = (not args.no_tc) and self.B >= 4 and ww.tc_workspace_bytes(max(self.nloc, 1), spec.m, self.B) > 0
+        layout = ww.LAYOUT_TILE32 if self.tc else ww.LAYOUT_COL4
+        nb = ww.packed_bytes(max(self.nloc, 1), spec.m, layout)
         self.R = max(1, int(np.ceil(4 * L2_BYTES / max(nb, 1))))
         planes = torch.empty((4, max(self.nloc, 1), spec.m), dtype=torch.int8, device=dev)
         for q in range(4):
             wi.codes_device(args.seed, q, self.nloc, spec.m, planes[q], spec.dist, row0=sh.row_begin)
-        base = ww.pack_ternary_device(planes)
+        base = ww.pack_ternary_device(planes, layout=layout)
         self.Wr = torch.empty((self.R, nb), dtype=torch.uint8, device=dev)
         self.Wr[:] = base
         sc = wi.scales(args.seed, spec.n, spec.per_row, spec.scale_lo, spec.scale_hi)
@@ -695,12 +699,9 @@ class _ReplicaLayer:
         self.S = torch.from_numpy(np.ascontiguousarray(sc)).to(dev)
         self.X = torch.from_numpy(wi.activations(args.seed, spec.m, self.B)).to(dev)
         self.Y = [torch.zeros(sh.n_padded * self.B, dtype=torch.complex64, device=dev)]
-        self.L = ww.Layer(self.nloc, spec.m, ww.LAYOUT_COL4,
+        self.L = ww.Layer(self.nloc, spec.m, layout,
                           ww.SCALES_PER_ROW if spec.per_row else ww.SCALES_PER_TENSOR,
                           ww.CONV_EQ1, 0 if args.no_pdl else ww.FLAG_PDL)
-        # batches of >= 4 vectors run on the tensor cores (ww_wl_gemv_batched_tc) unless --no-tc
-        self.tc = (not args.no_tc) and self.B >= 4 and ww.tc_workspace_bytes(self.nloc, spec.m, self.B) > 0
-        # zeroed once (ww.h: every call leaves the reduction words zeroed again)
         self.ws = (torch.zeros(ww.tc_workspace_bytes(self.nloc, spec.m, self.B) + 256, dtype=torch.uint8, device=dev)
                    if self.tc else None)
 

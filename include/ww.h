@@ -283,7 +283,8 @@ ww_status ww_program_run(const ww_program* prog, void* stream);
 
 /* Batched WL-GEMV on the tensor cores (tcgen05.mma kind::i8) for the small-batch variant
  * (BASELINE config 5): with B vectors the layer is a dense contraction of the stacked ternary
- * planes (4n x m, decoded in-kernel from COL4 to int8 in shared memory) with the B x 2 real
+ * planes (4n x m; L->layout must be WW_LAYOUT_TILE32, whose App. H words are decoded in-kernel
+ * to int8 in shared memory by a byte-permute table) with the B x 2 real
  * components of x, each split into three signed 8-bit limbs of a 22-bit fixed-point value
  * (scale 2^-E per vector and component, E from max |x|); int32 accumulation is exact, the
  * limbs are recombined in fp64 and the scales applied once per row (Eq. 1 /

@@ -34,6 +34,7 @@ constexpr int kDecodeWarps = 16;  // decode warps: one 16-column chunk of one ro
                                   // and block (warps 0-3 also run the epilogue)
 constexpr int kThreads = (kDecodeWarps + 1) * 32;  // + one MMA / limb-producer warp
 constexpr int kLimbs = 3;
+constexpr int kSlab32 = 2048;  // WW_LAYOUT_TILE32: one (32-row tile, 64-column slab) unit
 constexpr int kMaxB = 16;      // 2B (vector, component) columns per limb group of 32
 constexpr int kStages = 3;     // A decode slots (and packed words in flight per thread)
 constexpr int kBStages = 4;    // limb slots
@@ -209,9 +210,11 @@ __global__ void __launch_bounds__(kLimbThreads) tc_limbs_kernel(const float* __r
             const int32_t q1 = (q - l0) >> 8;
             const int32_t l1 = (int32_t)(int8_t)(q1 & 0xff);
             const int32_t l2 = (q1 - l1) >> 8;
-            L[0][i >> 2] |= ((uint32_t)l0 & 0xffu) << (8 * (i & 3));
-            L[1][i >> 2] |= ((uint32_t)l1 & 0xffu) << (8 * (i & 3));
-            L[2][i >> 2] |= ((uint32_t)l2 & 0xffu) << (8 * (i & 3));
+            // column i of the group sits at K position kp of the decoded A rows (decode_word)
+            const int kp = (i & 1) ? 8 + (i >> 1) : (i >> 1);
+            L[0][kp >> 2] |= ((uint32_t)l0 & 0xffu) << (8 * (kp & 3));
+            L[1][kp >> 2] |= ((uint32_t)l1 & 0xffu) << (8 * (kp & 3));
+            L[2][kp >> 2] |= ((uint32_t)l2 & 0xffu) << (8 * (kp & 3));
         }
 #pragma unroll
         for (int k = 0; k < kLimbs; ++k)
@@ -221,12 +224,12 @@ __global__ void __launch_bounds__(kLimbThreads) tc_limbs_kernel(const float* __r
 }
 
 struct TcParams {
-    const uint4* packed;  // COL4, n x W chunks
+    const uint8_t* packed;  // WW_LAYOUT_TILE32 (App. H words re-tiled)
     const float* scales;
     const int8_t* limbs;  // canonical B operand, kpad/32 K-steps of N x 32 bytes
     const int* expo;      // 2B exponents
     float* Y;
-    int64_t n, W, kpad, ldy;
+    int64_t n, S, kpad, ldy;  // S: 64-column slabs per row (TILE32)
     int32_t B, N, per_row, conv;
     int32_t splits;                // CTAs per 32-row tile (one cluster), each a contiguous share
                                    // of the K blocks
@@ -237,13 +240,19 @@ __device__ __forceinline__ void tc_trace(const TcParams& p, int kb, int ev) {
     if (p.trace && blockIdx.x < 2) p.trace[blockIdx.x * 512 + kb * 8 + ev] = clock64();  // SM cycles (CTAs 0, 1)
 }
 
-// int8 {-1, 0, +1} of plane p for the four columns of one COL4 word (byte = column, bits
-// 2p+1 = +1, 2p = -1): (pos bits) | (neg bits) * 0xFF, bytewise (pos and neg exclusive, no
-// carries between bytes)
-__device__ __forceinline__ uint32_t dec4(uint32_t w, int p) {
-    const uint32_t pos = (w >> (2 * p + 1)) & 0x01010101u;
-    const uint32_t neg = (w >> (2 * p)) & 0x01010101u;
-    return pos | (neg * 0xFFu);
+// One App. H word (16 codes of one plane and row, bit 2k = -1, bit 2k+1 = +1) -> 16 int8 in
+// the K order [0,2,4,6, 8,10,12,14, 1,3,5,7, 9,11,13,15] (the limbs use the same order): the
+// nibbles of w & 0x3333_3333 are the even codes, of (w >> 2) & 0x3333_3333 the odd ones, and
+// PRMT with a nibble selector picks byte `code` of the table {0x00, 0xFF, 0x01, 0x00} (the
+// unused code (1,1) gives 0, DESIGN R3)
+__device__ __forceinline__ void decode_word(uint32_t w, uint32_t* o) {
+    constexpr uint32_t kTable = 0x0001FF00u;
+    const uint32_t e = w & 0x33333333u;
+    const uint32_t d = (w >> 2) & 0x33333333u;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(o[0]) : "r"(kTable), "r"(e));
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(o[1]) : "r"(kTable), "r"(e >> 16));
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(o[2]) : "r"(kTable), "r"(d));
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(o[3]) : "r"(kTable), "r"(d >> 16));
 }
 
 __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constant__ TcParams p) {
@@ -343,24 +352,18 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
             }
         }
     } else {
-        // ---- decode warps.  Task of this thread: output row r of the tile, column chunk cc
-        // (16 columns) of the K block; its four planes are M rows 4r .. 4r+3 = four
-        // consecutive 16-byte rows of one core matrix.  Its packed words stream kStages blocks
-        // ahead in registers.
-        // warp w decodes rows 2w (even lanes) and 2w+1 (odd lanes), chunk = lane / 2: a
-        // phase of 8 lanes then covers both rows of a core-matrix pair and, with the plane
-        // order rotated by (lane / 2) % 4, all 8 of its 16-byte rows (conflict-free STS.128)
-        const int r = ((tid >> 5) << 1) | (lane & 1), cc = lane >> 1;
-        const int rot = (lane >> 1) & 3;
-        const int64_t grow = row0 + r;
-        const bool rok = grow < p.n;
-        const uint32_t a_off = (uint32_t)(cc >> 1) * (kTM * 32) + (uint32_t)(r >> 1) * 256u +
-                               (uint32_t)(cc & 1) * 128u + (uint32_t)((r & 1) * 4) * 16u;
-        const uint4* wsrc = p.packed + (rok ? grow : 0) * p.W + cc;
+        // ---- decode warps.  Task of this thread: M-row mr (= 4 (row % 32) + plane, the
+        // WW_LAYOUT_TILE32 order) and slab j (64 columns) of the K block: its 4 App. H words
+        // (16 bytes, one coalesced 512-byte request per warp) become 64 int8 by 16 PRMTs
+        // (decode_word) and 4 conflict-free STS.128 into the canonical K-major A tile.  The
+        // words stream kStages blocks ahead in registers.
+        const int mr = tid & 127, j = tid >> 7;
+        const uint32_t a_off = (uint32_t)(2 * j) * (kTM * 32) + (uint32_t)(mr >> 3) * 256u + (uint32_t)(mr & 7) * 16u;
+        const uint8_t* tsrc = p.packed + (int64_t)tile * p.S * kSlab32 + (int64_t)mr * 16;
         auto load_w = [&](int kb) -> uint4 {
-            const int64_t gk = (int64_t)(kb0 + kb);
-            const int64_t c = gk * (kKB / 16) + cc;
-            return (rok && kb < nkb && c < p.W) ? ldg_stream(wsrc + gk * (kKB / 16)) : make_uint4(0, 0, 0, 0);
+            const int64_t slab = (int64_t)(kb0 + kb) * (kKB / 64) + j;
+            return (kb < nkb && slab < p.S) ? ldg_stream(reinterpret_cast<const uint4*>(tsrc + slab * kSlab32))
+                                            : make_uint4(0, 0, 0, 0);
         };
         uint4 wq[kStages];
 #pragma unroll
@@ -378,10 +381,13 @@ __global__ void __launch_bounds__(kThreads, 1) wl_tc_kernel(const __grid_constan
             for (int i = 0; i < kStages - 1; ++i) wq[i] = wq[i + 1];
             wq[kStages - 1] = load_w(kb + kStages);
             const uint32_t dst = sa + (uint32_t)st * a_bytes + a_off;
+            // word i (columns 16 i .. 16 i + 15 of the slab): K step 2 j + i / 2, half i % 2
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int pl = (i + rot) & 3;
-                sts128(dst + 16u * pl, dec4(w.x, pl), dec4(w.y, pl), dec4(w.z, pl), dec4(w.w, pl));
+                uint32_t o[4];
+                decode_word(ws[i], o);
+                sts128(dst + (uint32_t)(i >> 1) * (kTM * 32) + (uint32_t)(i & 1) * 128u, o[0], o[1], o[2], o[3]);
             }
             fence_proxy_async_smem();  // this thread's generic stores -> the async proxy
             __syncwarp();
@@ -515,8 +521,8 @@ extern "C" ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed
         return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: null pointer", fn);
     if (L->n < 1 || L->m < 1 || L->n > ((int64_t)1 << 30) || L->m > kLimbMaxM)
         return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: n=%lld m=%lld", fn, (long long)L->n, (long long)L->m);
-    if (L->layout != WW_LAYOUT_COL4)
-        return ww::fail(WW_ERR_UNSUPPORTED, "%s: needs WW_LAYOUT_COL4", fn);
+    if (L->layout != WW_LAYOUT_TILE32)
+        return ww::fail(WW_ERR_UNSUPPORTED, "%s: needs WW_LAYOUT_TILE32", fn);
     if (L->conv != WW_CONV_EQ1 && L->conv != WW_CONV_ALG1)
         return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: conv %d", fn, L->conv);
     if (B < 1 || B > kMaxB)
@@ -537,13 +543,13 @@ extern "C" ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed
     if (e != cudaSuccess) return ww::fail(WW_ERR_CUDA, "%s: %s", fn, cudaGetErrorString(e));
     TcParams p;
     memset(&p, 0, sizeof p);
-    p.packed = reinterpret_cast<const uint4*>(packed_d);
+    p.packed = reinterpret_cast<const uint8_t*>(packed_d);
     p.scales = scales_d;
     p.limbs = limbs;
     p.expo = expo;
     p.Y = Y_d;
     p.n = L->n;
-    p.W = ww::words_per_row(L->m);
+    p.S = ww::tile32_slabs(L->m);
     p.kpad = kpad;
     p.ldy = ldy;
     p.B = B;

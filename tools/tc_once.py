@@ -12,12 +12,12 @@ n, m, B = 2048, 5504, int(sys.argv[1]) if len(sys.argv) > 1 else 16
 planes = torch.empty((4, n, m), dtype=torch.int8, device="cuda")
 for q in range(4):
     wi.codes_device(1, q, n, m, planes[q])
-packed = ww.pack_ternary_device(planes)
+packed = ww.pack_ternary_device(planes, layout=ww.LAYOUT_TILE32)
 sc = torch.rand((n, 4), device="cuda") * 0.09 + 0.01
 X = torch.randn((B, m), dtype=torch.complex64, device="cuda")
 ws = torch.zeros(ww.tc_workspace_bytes(n, m, B) + 256, dtype=torch.uint8, device="cuda")
 for _ in range(3):
-    ww.wl_gemv_batched_tc(ww.Layer(n, m), packed, sc, X, workspace=ws)
+    ww.wl_gemv_batched_tc(ww.Layer(n, m, ww.LAYOUT_TILE32), packed, sc, X, workspace=ws)
 torch.cuda.synchronize()
 print("ok")
 if "--trace" in sys.argv:
@@ -26,7 +26,7 @@ if "--trace" in sys.argv:
     tr = torch.zeros(64 * 8 * 8, dtype=torch.int64, device="cuda")
     ww._lib.ww_debug_tc_trace.argtypes = [ctypes.c_void_p]
     ww._lib.ww_debug_tc_trace(tr.data_ptr())
-    ww.wl_gemv_batched_tc(ww.Layer(n, m), packed, sc, X, workspace=ws)
+    ww.wl_gemv_batched_tc(ww.Layer(n, m, ww.LAYOUT_TILE32), packed, sc, X, workspace=ws)
     torch.cuda.synchronize()
     ww._lib.ww_debug_tc_trace(None)
     t = tr.view(-1, 8).cpu().numpy().astype(np.float64)

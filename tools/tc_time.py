@@ -19,9 +19,13 @@ def main(n=2048, m=5504, batches=(1, 2, 4, 8, 16)):
     for q in range(4):
         wi.codes_device(1, q, n, m, planes[q])
     base = ww.pack_ternary_device(planes)
+    t32 = ww.pack_ternary_device(planes, layout=ww.LAYOUT_TILE32)  # the tensor-core path's layout
     del planes
     reps = torch.empty((R, nb), dtype=torch.uint8, device="cuda")
     reps[:] = base
+    rept = torch.empty((R, t32.numel()), dtype=torch.uint8, device="cuda")
+    rept[:] = t32
+    Lt = ww.Layer(n, m, ww.LAYOUT_TILE32)
     sc = torch.rand((n, 4), device="cuda") * 0.09 + 0.01
     L = ww.Layer(n, m)
     s = torch.cuda.Stream()
@@ -51,7 +55,7 @@ def main(n=2048, m=5504, batches=(1, 2, 4, 8, 16)):
         X = torch.randn((B, m), dtype=torch.complex64, device="cuda")
         Y = torch.empty((B, n), dtype=torch.complex64, device="cuda")
         ws = torch.zeros(ww.tc_workspace_bytes(n, m, B) + 256, dtype=torch.uint8, device="cuda")
-        t_tc = run(lambda r: ww.wl_gemv_batched_tc(L, reps[r], sc, X, Y, ws, stream=s))
+        t_tc = run(lambda r: ww.wl_gemv_batched_tc(Lt, rept[r], sc, X, Y, ws, stream=s))
         t_fa = run(lambda r: ww.wl_gemv_batched(L, reps[r], sc, X, Y, stream=s)) if B <= 16 else float("nan")
         bytes_ = nb + 8 * m * B
         print(f"{n}x{m} B={B:2d}: tensor-core {t_tc:8.2f} us ({bytes_ / t_tc * 1e-3:7.0f} GB/s)   "

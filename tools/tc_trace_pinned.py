@@ -6,14 +6,20 @@ import ctypes, sys, time, threading, numpy as np, torch
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import paper_2604_20913_b200 as ww, ww_inputs as wi
 from _wl import LayerCase
-case = LayerCase(300, 517, seed=3, B=8).device(ww, torch)
+def _t32(c):
+    c.device(ww, torch)
+    c.packed_d = torch.from_numpy(ww.pack_ternary(c.planes, ww.LAYOUT_TILE32).view(np.uint8)).cuda()
+    return c
+
+
+case = _t32(LayerCase(300, 517, seed=3, B=8))
 buf = torch.zeros(2 * 64 * 8, dtype=torch.int64).pin_memory()
 ww._lib.ww_debug_tc_trace(ctypes.c_void_p(buf.data_ptr()))
-L = case.layer(ww, ww.CONV_EQ1)
+L = ww.Layer(case.n, case.m, ww.LAYOUT_TILE32)
 n_arg = sys.argv[1:] and sys.argv[1]
 if n_arg == "big":
-    case = LayerCase.from_spec(wi.C3B, seed=5, B=8).device(ww, torch)
-    L = case.layer(ww, ww.CONV_EQ1)
+    case = _t32(LayerCase.from_spec(wi.C3B, seed=5, B=8))
+    L = ww.Layer(case.n, case.m, ww.LAYOUT_TILE32)
 y = ww.wl_gemv_batched_tc(L, case.packed_d, case.scales_d, case.x_d)
 done = []
 th = threading.Thread(target=lambda: (torch.cuda.synchronize(), done.append(1)), daemon=True)
