@@ -161,12 +161,17 @@ ww_status ww_shard_plan(int64_t n, int64_t m, int32_t world, int32_t rank, ww_sh
 
 /* Launch configuration the GPU entry points use for (L, B): grid (one CTA per SM, each
  * owning a contiguous row range), block, dynamic shared memory, the number of x column
- * tiles and their width (16-column chunks), the SM count it was planned for, the column
- * parts of a row (always 1 and split_chunks = W = ceil(m/16) in this version: a row is
- * one warp's work unit, swept 32 chunks at a time) and the path (0 = single x tile; 1 =
- * column tiles with row waves, taken when x or the CTA's row totals do not fit shared
- * memory).  A row's accumulation order is a function of (m, B) only, so results never
- * depend on n, the shard or the grid.  Pure host function. */
+ * tiles and their width (16-column chunks), the SM count it was planned for, the parts
+ * of a row and the path (0 = single x tile; 1 = column tiles with row waves, taken when x
+ * or the CTA's row totals do not fit shared memory).  parts = 1: a row is one warp's work
+ * unit, swept 32 chunks at a time (split_chunks = W = ceil(m/16)).  parts = 2 (B = 1, path
+ * 0, J = ceil(W/32) >= 2, chosen when it shortens the busiest SM sub-partition's share by
+ * >= 4 %): rows are cut after split_chunks = 32 ceil(J/2) chunks into halves dealt out to
+ * the warps like rows, and a first half's lane accumulators are handed through shared
+ * memory to the warp that sweeps the second half, so the row is still accumulated in
+ * whole-row order (same bits).  A row's accumulation order is a function of (m, B) only,
+ * so results never depend on n, the shard, the grid or the parts.  Pure host function
+ * (the SM count comes from the current device, 148 without one). */
 typedef struct {
     int32_t grid, block, smem_bytes, tiles, tile_chunks, num_sms, parts, split_chunks, path;
 } ww_launch_info;

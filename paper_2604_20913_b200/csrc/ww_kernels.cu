@@ -24,6 +24,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "ww.h"
 #include "ww_internal.h"
@@ -50,6 +51,8 @@ constexpr int kXBudgetBytes = 184 * 1024;  // x tile per CTA (multi-tile path)
 constexpr int kGroup = 4;                  // batches above this run as groups of 4 vectors
 constexpr int64_t kSmemBudget = 226 * 1024; // single-tile path: all shared memory of a CTA
 constexpr int kPrefetch = 2;                 // L2 prefetch distance beyond the weight loads
+// bytes of one lane's accumulator state handed between warps (split rows, B = 1 only)
+constexpr int kHandLaneBytes = (int)sizeof(Acc<1>);  // 2 column-parity sets x 4 planes x float2
 
 #if WW_DEBUG_FLAGS
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -93,6 +96,8 @@ struct alignas(64) Params {
     int32_t single;       // 1: single x tile path (ww_launch_info.path == 0)
     int32_t J;            // single-tile path: 32-chunk sweeps (= x slices) per row
     int32_t rows_cap;     // single-tile path: rows per CTA the shared totals / scales hold
+    int32_t split;        // single tile, B = 1: rows cut in two halves handed between warps
+                          // (ww_launch_info.parts == 2)
     int32_t dbg;          // tools only (ww_debug_set_flags): 1 = skip griddepcontrol.wait,
                           // bits 8..: trace slot (WW_TRACE builds),
                           // 2 = skip the accumulation, 8 = bulk L2 prefetch of the CTA's
@@ -224,16 +229,44 @@ __device__ __forceinline__ void epilogue(const Params& p, const float* T0, int64
     __syncwarp();
 }
 
+// Split-row hand-off of one lane's accumulator state (B = 1): float4 i of the lane at
+// addr + 512 i (32 lanes x 16 B per step: conflict-free), published by the 32 lanes'
+// mbarrier arrivals (release) and read after the receiver's wait (acquire).
+template <int B>
+__device__ __forceinline__ void hand_store(const Acc<B>& acc, uint32_t addr) {
+    const float2* a = &acc.a[0][0][0][0];
+#pragma unroll
+    for (int i = 0; i < (int)sizeof(Acc<B>) / 16; ++i)
+        sts128_f4(addr + 512u * i, make_float4(a[2 * i].x, a[2 * i].y, a[2 * i + 1].x, a[2 * i + 1].y));
+}
+template <int B>
+__device__ __forceinline__ void hand_load(Acc<B>& acc, uint32_t addr) {
+    float2* a = &acc.a[0][0][0][0];
+#pragma unroll
+    for (int i = 0; i < (int)sizeof(Acc<B>) / 16; ++i) {
+        const float4 v = lds128(addr + 512u * i);
+        a[2 * i] = make_float2(v.x, v.y);
+        a[2 * i + 1] = make_float2(v.z, v.w);
+    }
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 // Shared-memory carve-up (bytes), identical on host (plan) and device.
 struct SmemLayout {
-    int64_t x_bytes, scratch_off, tot_off, scale_off, bar_off, total;
+    int64_t x_bytes, scratch_off, tot_off, scale_off, bar_off, hand_off, hbar_off, desc_off, total;
 };
+
 // x first (1024-B aligned for the 128B-swizzled TMA boxes), then per-warp reduction scratch
 // (multi-tile path), then -- single tile only -- the reduced totals of every CTA row
 // ([rows][NV] floats), the CTA's row scales and one mbarrier per x slice.
 // Single tile: x_chunks = 32*J per vector; multi-tile: the tile width.
+// Split rows (single tile, B = 1): one hand-off slot of 32 lane states per warp, then one
+// mbarrier per warp.
 __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps, bool single,
-                                                  int nbars, int rows, bool x2 = false) {
+                                                  int nbars, int rows, bool x2 = false,
+                                                  bool split = false) {
     const int64_t nv = next_pow2(8 * B);
     SmemLayout L;
     L.x_bytes = (int64_t)B * x_chunks * 128;
@@ -243,7 +276,10 @@ __host__ __device__ inline SmemLayout smem_layout(int B, int x_chunks, int warps
     L.scale_off = L.tot_off + (single ? (int64_t)rows * nv * 4 : 0);
     // scales: one 16-B slot per CTA row (per-row mode) or per warp (per-tensor mode)
     L.bar_off = L.scale_off + (single ? 16 * (int64_t)(rows > warps ? rows : warps) : 0);
-    L.total = L.bar_off + (single ? 8 * (int64_t)nbars : 0) + 1024;  // + base alignment slack
+    L.hand_off = (L.bar_off + (single ? 8 * (int64_t)nbars : 0) + 15) / 16 * 16;
+    L.hbar_off = L.hand_off + (split ? (int64_t)warps * 32 * kHandLaneBytes : 0);
+    L.desc_off = L.hbar_off + (split ? 8 * (int64_t)warps : 0);  // 16-B per-warp descriptors
+    L.total = L.desc_off + (split ? 16 * (int64_t)warps : 0) + 1024;  // + base alignment slack
     return L;
 }
 
@@ -267,7 +303,7 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
     const bool single = p.single != 0;
     const int nbars = single ? p.J : 0;
     const SmemLayout SL = smem_layout(B, single ? 32 * p.J : p.x_stride, nwarps, single, nbars,
-                                      p.rows_cap, p.pro == WW_PRO_MUL);
+                                      p.rows_cap, p.pro == WW_PRO_MUL, B == 1 && p.split);
     float* part = reinterpret_cast<float*>(smem + SL.scratch_off - 128);  // [32]
     float* sc = reinterpret_cast<float*>(smem + SL.scratch_off) + warp * NV;
     const uint32_t bars = xs + (uint32_t)SL.bar_off;
@@ -280,6 +316,8 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
         // thread is measurably slow)
         for (int j = threadIdx.x; j < nbars; j += blockDim.x)
             mbar_init(bars + 8 * j, p.use_tma ? 1u : blockDim.x);
+        if (B == 1 && p.split && threadIdx.x < nwarps)  // hand-off barriers: 32 lane arrivals
+            mbar_init(xs + (uint32_t)SL.hbar_off + 8u * threadIdx.x, 32u);
         fence_barrier_init();
     }
 
@@ -351,12 +389,89 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             ++pk;
             return w;
         };
+        // Split rows (p.split, B = 1): the CTA's rows are cut into 2 NRc half
+        // units (row u >> 1, sweeps [0, h) or [h, J), h = ceil(J/2)) and the units are dealt
+        // out like rows, so the four sub-partitions get equal work to +-1 half row.  A warp
+        // whose range ends with a first half (giver) sweeps it first and hands its lane state
+        // to the next warp through shared memory; a warp whose range starts with a second half
+        // (receiver) sweeps it last, continuing from that state -- no warp waits on a later
+        // one, and a row's accumulation order is the whole-row order.
+        const int hJ = (J + 1) / 2;
+        // the warp's split geometry {mr0, mr1, giver | receiver << 1, nseg} lives in shared
+        // memory and is re-read at each (rare) segment change, so it holds no registers
+        // across the sweep loop
+        const uint32_t desc = xs + (uint32_t)SL.desc_off + 16u * warp;
+        int er0 = w0, er1 = w1;  // rows whose epilogue this warp runs (scales copied)
+        bool has_work = w0 < w1;
+        if (B == 1 && p.split) {
+            const int NU = 2 * NRc;
+            const int uub = NU / nwarps, uue = NU - uub * nwarps;
+            const int u0 = warp * uub + (warp < uue ? warp : uue);
+            const int u1 = u0 + uub + (warp < uue ? 1 : 0);
+            const bool giv = u1 > u0 && ((u1 - 1) & 1) == 0;
+            const bool rcv = u1 > u0 && (u0 & 1) == 1;
+            const int mr0 = (u0 + (rcv ? 1 : 0)) >> 1, mr1 = (u1 - (giv ? 1 : 0)) >> 1;
+            const int nseg = (giv ? 1 : 0) + (mr1 - mr0) + (rcv ? 1 : 0);
+            if (lane == 0)
+                asm volatile("st.shared.v4.s32 [%0], {%1,%2,%3,%4};" ::"r"(desc), "r"(mr0), "r"(mr1),
+                             "r"((giv ? 1 : 0) | (rcv ? 2 : 0)), "r"(nseg)
+                             : "memory");
+            __syncwarp();
+            er0 = rcv ? mr0 - 1 : mr0;
+            er1 = mr1;
+            has_work = nseg > 0;
+        }
+        struct Seg {
+            int row, kb, ke, kind;  // kind: 0 giver half, 1 whole row, 2 receiver half
+        };
+        auto seg_of = [&](int i, int& nseg) -> Seg {
+            int mr0, mr1, fl;
+            asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(mr0), "=r"(mr1), "=r"(fl), "=r"(nseg)
+                         : "r"(desc)
+                         : "memory");
+            const int g = fl & 1;
+            if (g && i == 0) return Seg{mr1, 0, hJ, 0};
+            if (i - g < mr1 - mr0) return Seg{mr0 + i - g, 0, J, 1};
+            return Seg{mr0 - 1, hJ, J, 2};
+        };
+        // segmented producer (split rows): sweeps of the segments in processing order, the
+        // L2 prefetch kPrefetch sweeps ahead inside a segment as in the stream producer
+        int spi = 0, spk = 0, spke = 0, skv = 0;
+        const uint4* sptr = p.packed;
+        if (B == 1 && p.split && has_work) {
+            int ns;
+            const Seg sg = seg_of(0, ns);
+            spk = sg.kb;
+            spke = sg.ke;
+            skv = spke < kvl ? spke : kvl;
+            sptr = p.packed + (r0 + sg.row) * p.W + lane + 32 * spk;
+        }
+        auto load_seg = [&]() -> uint4 {
+            prefetch_chunk_lt(sptr + 32 * kPrefetch, spk + kPrefetch, skv);
+            const uint4 w = ldg_stream_lt(sptr, spk, skv);
+            sptr += 32;
+            if (++spk == spke) {
+                int ns;
+                const Seg sg = seg_of(++spi, ns);
+                if (spi < ns) {
+                    const int kv = (threadIdx.x & 31) < (int)p.W - 32 * (p.J - 1) ? p.J : p.J - 1;
+                    spk = sg.kb;
+                    spke = sg.ke;
+                    skv = spke < kv ? spke : kv;
+                    sptr = p.packed + (r0 + sg.row) * p.W + (threadIdx.x & 31) + 32 * spk;
+                } else {
+                    skv = 0;
+                }
+            }
+            return w;
+        };
         float* tot = reinterpret_cast<float*>(smem + SL.tot_off);  // [rows][NV]
         float4 gam[kGammaRegs];  // WW_PRO_RMSNORM: this thread's gamma (a weight), pre-wait
         if (B == 1 && p.pro == WW_PRO_RMSNORM)
             gamma_prefetch(gam, p.gamma, p.m, J, threadIdx.x, blockDim.x);
         float rnorm = 1.0f;  // RMSNorm factor, applied in the epilogue
-        auto run = [&](auto&& load_next) {
+        auto run = [&](auto&& load_next, auto split_tag) {
             uint4 qa = load_next(), qb = load_next();
             __syncthreads();  // mbarrier inits visible
             trace(tslot, 1);
@@ -389,9 +504,9 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
             {
                 const uint32_t sdst = xs + (uint32_t)SL.scale_off;
                 if (p.per_row_scales) {
-                    const float* src = p.scales + 4 * (r0 + w0);
-                    const int ns = 4 * (w1 - w0);
-                    for (int i = lane; i < ns; i += 32) cp_async4(sdst + 16u * w0 + 4u * i, src + i);
+                    const float* src = p.scales + 4 * (r0 + er0);
+                    const int ns = 4 * (er1 - er0);
+                    for (int i = lane; i < ns; i += 32) cp_async4(sdst + 16u * er0 + 4u * i, src + i);
                 } else if (lane < 4) {
                     cp_async4(sdst + 16u * warp + 4u * lane, p.scales + lane);
                 }
@@ -417,9 +532,65 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 }
                 __syncthreads();
                 if (p.pro == WW_PRO_RMSNORM) rnorm = rms_factor(part, nwarps, p.m, p.eps);
-            } else if (w0 < w1 && !(WW_X_LDG && B == 1 && p.use_tma)) {  // x slices in before
+            } else if (has_work && !(WW_X_LDG && B == 1 && p.use_tma)) {  // x slices in before
                 for (int j = 0; j < J; ++j) mbar_wait0(bars + 8 * j);     // the warp's first sweep
             }
+            if constexpr (decltype(split_tag)::value) {
+                // split rows: segments in processing order (giver half, whole rows, receiver
+                // half); the lane state of a row's first half continues in the next warp, so
+                // every row is accumulated sweep 0..J-1 in order, exactly as a whole row
+                const uint32_t hand = xs + (uint32_t)SL.hand_off;
+                const uint32_t hbar = xs + (uint32_t)SL.hbar_off;
+                bool scales_ready = false;
+                int nseg = has_work ? 1 : 0;
+#pragma unroll 1
+                for (int i = 0; i < nseg; ++i) {
+                    const Seg sg = seg_of(i, nseg);
+                    const int row = sg.row, kb = sg.kb, ke = sg.ke;
+                    const bool is_giv = sg.kind == 0, is_rcv = sg.kind == 2;
+                    float2 res = make_float2(0.f, 0.f);
+                    if (B == 1 && p.epi == WW_EPI_RESIDUAL && lane == 0 && !is_giv)
+                        res = __ldcg(reinterpret_cast<const float2*>(p.residual) + p.row0 + r0 + row);
+                    if (is_rcv) {  // the previous warp's state after sweeps [0, h) of this row
+                        mbar_wait0(hbar + 8u * (warp - 1));
+                        const uint32_t src = hand + (uint32_t)(warp - 1) * 32u * kHandLaneBytes;
+                        hand_load(acc, src + 16u * lane);
+                    }
+                    uint32_t xc = xb + 4096u * (uint32_t)kb;
+#pragma unroll 1
+                    for (int k = kb; k < ke; ++k) {
+                        const uint4 cur = qa;
+                        qa = qb;
+                        qb = load_next();
+                        chunk<B>(acc, cur, xc, bstride);
+                        xc += 4096u;
+                    }
+                    if (is_giv) {  // hand the lane state to the next warp
+                        hand_store(acc, hand + (uint32_t)warp * 32u * kHandLaneBytes + 16u * lane);
+                        mbar_arrive(hbar + 8u * warp);
+                        acc.zero();
+                        continue;
+                    }
+                    reduce_to<B>(acc, tot + row * NV);
+                    if (!scales_ready) {
+                        cp_async_wait_all();
+                        __syncwarp();
+                        scales_ready = true;
+                    }
+                    if (lane < B) {
+                        float T[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) T[q] = tot[row * NV + 8 * lane + q];
+                        const float* sr = reinterpret_cast<const float*>(smem + SL.scale_off) +
+                                          4 * (p.per_row_scales ? row : warp);
+                        if (B == 1 && (p.epi != WW_EPI_NONE || p.pro == WW_PRO_RMSNORM))
+                            store_y_ops(p, T, sr, r0 + row, res, rnorm);
+                        else
+                            store_y(p, T, sr, lane, r0 + row);
+                    }
+                    acc.zero();
+                }
+            } else {
 #pragma unroll 1
             for (int r = w0; r < w1; ++r) {
                 uint32_t xc = xb;
@@ -485,11 +656,21 @@ wl_gemv_kernel(const __grid_constant__ Params p) {
                 if (tr_sweep < 29) trace(tslot, tr_sweep++);
                 acc.zero();
             }
+            }
         };
-        if constexpr (kStream)
-            run(load_stream);
-        else
-            run(load_rows);
+        bool ran = false;
+        if constexpr (B == 1) {
+            if (p.split) {
+                run(load_seg, std::true_type{});
+                ran = true;
+            }
+        }
+        if (!ran) {
+            if constexpr (kStream)
+                run(load_stream, std::false_type{});
+            else
+                run(load_rows, std::false_type{});
+        }
         trace(tslot, 29);  // sweeps done
         trace(tslot, 31);
         return;
@@ -568,6 +749,9 @@ __global__ void pack_col4_kernel(const int8_t* __restrict__ planes, int64_t n, i
 // ------------------------------------------------------------------ launch configuration
 int num_sms() { return ww::device_sms(); }
 
+// tests: -1 = planner decides, 0 / 1 = force whole / split rows (B = 1, single tile, J >= 2)
+std::atomic<int> g_force_split{-1};
+
 ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
     const int64_t W = ww::words_per_row(L->m);
     const int warps = warps_for_b(B);
@@ -594,6 +778,28 @@ ww_status plan(const ww_layer* L, int32_t B, int sms, ww_launch_info* li) {
         li->split_chunks = (int32_t)W;
         li->smem_bytes = (int32_t)single_bytes;
         li->path = 0;
+        // B = 1: cut rows into two halves handed between warps when that shortens the
+        // busiest SM sub-partition's share by >= 4 % (n = 2048 shapes: 14 rows per CTA on 16
+        // warps leave sub-partitions with 4 + 4 + 3 + 3 rows; halves give 7 + 7 + 7 + 7).
+        // Results are bitwise the same either way (the hand-off keeps the row's order).
+        // Only for rows of a ragged last sweep (W % 32 != 0, the row-by-row producer): where
+        // W = 32 J the whole-row stream producer (no row transitions) measured faster than
+        // halves on every config-4 shape.
+        if (B == 1 && T >= 2 && (W % 32 != 0 || g_force_split.load() == 1)) {
+            const int sp = warps / 4;  // warps per sub-partition
+            const double whole = (double)((rows + 4 - 1) / 4) * T;
+            const double halves = (double)((2 * rows + 4 - 1) / 4) * 0.5 * T;
+            const int force = g_force_split.load();
+            const bool split = force >= 0 ? force != 0 : (sp >= 1 && halves <= 0.96 * whole);
+            const int64_t split_bytes =
+                smem_layout(B, (int)(32 * T), warps, true, (int)T,
+                            (int)std::min<int64_t>(rows, 1 << 20), false, true).total;
+            if (split && split_bytes <= kSmemBudget) {
+                li->parts = 2;
+                li->split_chunks = (int32_t)((T + 1) / 2 * 32);
+                li->smem_bytes = (int32_t)split_bytes;
+            }
+        }
         return WW_OK;
     }
     // x (or the CTA's row totals) does not fit one tile: column tiles of whole 32-chunk
@@ -680,6 +886,8 @@ extern "C" void ww_debug_force_cp_async(int on) { g_force_cp_async = on != 0; }
 // Not part of the ABI: tests compare the two producer instantiations (kStream / row by row).
 extern "C" void ww_debug_force_rows(int on) { g_force_rows = on != 0; }
 extern "C" int ww_debug_last_stream(void) { return g_last_stream; }
+// Not part of the ABI: tests compare split and whole rows (-1 = the planner's choice).
+extern "C" void ww_debug_force_split(int mode) { g_force_split = mode < 0 ? -1 : (mode != 0); }
 // Not part of the ABI: overhead-measurement switches for tools/chain_time.py (Params::dbg).
 extern "C" void ww_debug_set_flags(int flags) { g_debug_flags = flags; }
 // Not part of the ABI: 1 if the last WL-GEMV launch staged x with TMA, 0 cp.async, -1 none yet.
@@ -725,7 +933,9 @@ ww_status launch_batch(const ww_layer* L, const void* packed_d, const float* sca
             const int64_t T = (ww::words_per_row(L->m) + 31) / 32;
             const int64_t rows = (L->n + li.grid - 1) / li.grid;
             const int64_t bytes =
-                smem_layout(1, (int)(32 * T), li.block / 32, true, (int)T, (int)rows, true).total;
+                smem_layout(1, (int)(32 * T), li.block / 32, true, (int)T, (int)rows, true,
+                            li.parts == 2)
+                    .total;
             if (bytes > kSmemBudget)
                 return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv_fused: x and x2 of m=%lld do not fit",
                                 (long long)L->m);
@@ -752,6 +962,7 @@ ww_status launch_batch(const ww_layer* L, const void* packed_d, const float* sca
     p.aligned16 = (((uintptr_t)X_d & 15) == 0) && (ldx % 2 == 0);
     p.x_stride = (li.tile_chunks + 31) / 32 * 32;
     p.single = li.path == 0;
+    p.split = li.parts == 2 ? 1 : 0;
     p.use_tma = p.single && (ops || !g_force_cp_async) ? (encode_x_map(p, B) ? 1 : 0) : 0;
     if (ops && !p.use_tma)
         return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv_fused: needs TMA staging (16 | m, 16-B x)");

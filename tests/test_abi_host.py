@@ -167,15 +167,36 @@ def test_query_launch_shapes():
         ww.query_launch(ww.Layer(8, 8, layout=ww.LAYOUT_PLANAR), 1)
 
 
-def test_launch_rows_are_whole_units():
-    # rows are never split into column parts (ww.h ww_launch_info), so a row's arithmetic
-    # depends on (m, B) only
+def test_launch_rows_whole_or_split_in_halves():
+    # rows are never split into column parts with their own sums (ww.h ww_launch_info): a
+    # row is either one warp's unit, or (B = 1, parts = 2) two halves whose lane state is
+    # handed from one warp to the next, so a row's arithmetic depends on (m, B) only
     for m in (16, 1000, 1024, 2048, 4096, 5504):
         W = -(-m // 16)
+        J = -(-W // 32)
         for B in (1, 4, 16):
             for n in (1, 148, 2048, 11008):
                 i = ww.query_launch(ww.Layer(n, m), B)
-                assert (i["parts"], i["split_chunks"]) == (1, W)
+                if i["parts"] == 1:
+                    assert i["split_chunks"] == W
+                else:
+                    assert (B, i["parts"], i["split_chunks"]) == (1, 2, -(-J // 2) * 32)
+                    assert J >= 2
+
+
+def test_split_rows_planned_where_sub_partitions_are_unbalanced():
+    # 148 SMs x 4 sub-partitions of 4 warps: n = 2048 gives 14 rows per CTA (4 + 4 + 3 + 3 per
+    # sub-partition) -> halves, for rows with a ragged last sweep (W % 32 != 0: down); rows
+    # of whole sweeps keep the stream producer; gate/up-like row counts stay whole
+    shapes = ((2048, 2048), (2048, 5504), (6144, 2048), (11008, 2048), (1, 2048), (1, 5504),
+              (2048, 3000), (11008, 3000))
+    parts = {(n, m): ww.query_launch(ww.Layer(n, m), 1)["parts"] for n, m in shapes}
+    if ww.query_launch(ww.Layer(2048, 2048), 1)["num_sms"] != 148:
+        pytest.skip("planned for another SM count")
+    assert parts == {(2048, 2048): 1, (2048, 5504): 2, (6144, 2048): 1, (11008, 2048): 1,
+                     (1, 2048): 1, (1, 5504): 2, (2048, 3000): 2, (11008, 3000): 1}
+    assert ww.query_launch(ww.Layer(2048, 5504), 2)["parts"] == 1
+    assert ww.query_launch(ww.Layer(2048, 500), 1)["parts"] == 1  # one sweep per row
 
 
 # ---------------------------------------------------------------- WW_LAYOUT_TILE32

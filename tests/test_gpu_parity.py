@@ -388,3 +388,31 @@ def test_keep_in_l2_window_leaves_results_unchanged():
     ww.keep_in_l2(None, s)
     torch.cuda.synchronize()
     assert torch.equal(y0, y1)
+
+
+SPLIT_SHAPES = [(2048, 2048), (2048, 5504), (6144, 2048), (1, 2048), (2, 1000), (149, 1000),
+                (300, 513), (17, 4097), (150, 1536), (37, 700), (2000, 3000)]
+
+
+@pytest.mark.parametrize("n,m", SPLIT_SHAPES)
+@pytest.mark.parametrize("per_row", [True, False])
+def test_split_rows_bitwise_equal_whole_rows(n, m, per_row):
+    # parts = 2 (ww.h ww_launch_info): halves of a row on two warps with the first half's
+    # lane state handed over in shared memory -- the same bits as the whole-row kernel on
+    # every shape (odd and even sweep counts, ragged last sweeps, a warp that is giver and
+    # receiver, n = 1), both x-staging paths
+    case = LayerCase(n, m, seed=n * 31 + m, per_row=per_row, lo=0.5, hi=2.0).device(ww, torch)
+    outs = {}
+    try:
+        for mode in (0, 1):
+            ww._lib.ww_debug_force_split(mode)
+            assert ww.query_launch(case.layer(ww, 0), 1)["parts"] == (2 if mode else 1)
+            outs[mode] = case.gpu(ww, torch, ww.CONV_EQ1)
+        ww._lib.ww_debug_force_cp_async(1)
+        outs["cpa"] = case.gpu(ww, torch, ww.CONV_EQ1)
+    finally:
+        ww._lib.ww_debug_force_split(-1)
+        ww._lib.ww_debug_force_cp_async(0)
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs["cpa"])
+    assert_parity(outs[1], case.oracle(orc.CONV_EQ1), case)

@@ -65,6 +65,18 @@ if __name__ == "__main__":
                     print(f"m={m} rows/SM={k:3d} pdl={flags}: {us:8.2f} us  "
                           f"({tcodes*1e12/148/1.965e9:5.1f} codes/clk/SM)", flush=True)
         sys.exit(0)
+    if "--split" in sys.argv:  # whole rows (stream / row-by-row producer) vs split halves
+        lib = ww._lib
+        for (n, m) in ((6144, 2048), (2048, 2048), (11008, 2048), (2048, 5504), (5504, 2048)):
+            for name, split, rows in (("whole", 0, 0), ("whole-rows", 0, 1), ("split", 1, 0)):
+                lib.ww_debug_force_split(split)
+                lib.ww_debug_force_rows(rows)
+                r = [time_shape(n, m, 1, flags=ww.FLAG_PDL)[0] for _ in range(3)]
+                print(f"n={n} m={m} {name:10s}: {min(r):.3f} us (runs {', '.join(f'{v:.3f}' for v in r)})",
+                      flush=True)
+        lib.ww_debug_force_split(-1)
+        lib.ww_debug_force_rows(0)
+        sys.exit(0)
     if "--warm" in sys.argv:
         for (n, m) in ((2048, 2048), (5504, 2048), (2048, 5504)):
             for flags in (0, ww.FLAG_PDL):
