@@ -195,16 +195,7 @@ __global__ void combine_kernel(const float* __restrict__ A, const float* __restr
     }
 }
 
-int sm_count() {
-    static int c = 0;
-    if (!c) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || c <= 0)
-            c = 148;
-    }
-    return c;
-}
+int sm_count() { return ww::device_sms(); }  // cached per device (ww_device.cu)
 
 template <typename K, typename... A>
 cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
@@ -240,14 +231,10 @@ extern "C" ww_status ww_ternary_gemv_plane(int64_t n, int64_t m, const void* pla
     const size_t smem = (size_t)Wp * 16 * 4;
     if (smem > 200 * 1024)
         return ww::fail(WW_ERR_UNSUPPORTED, "ww_ternary_gemv_plane: m=%lld too large", (long long)m);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(tern_plane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        cudaFuncSetAttribute(tern_plane_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)cudaSharedmemCarveoutMaxShared);
-        attr = true;
-    }
+    // the 32-bit kernel is launched only when the 128-bit one below does not apply
+    const auto prepare32 = [] {
+        return ww::prepare_kernel(reinterpret_cast<const void*>(tern_plane_kernel), 200 * 1024);
+    };
     const uint32_t* pl = reinterpret_cast<const uint32_t*>(planar_d) + (int64_t)plane * n * W;
     const int grid = (int)std::min<int64_t>(sm_count(), n);
     if (W % 4 == 0 && ((uintptr_t)planar_d & 15) == 0) {  // the 128-bit kernel
@@ -267,6 +254,9 @@ extern "C" ww_status ww_ternary_gemv_plane(int64_t n, int64_t m, const void* pla
             return ww::ok();
         }
     }
+    if (const int e32 = prepare32())
+        return ww::fail(WW_ERR_CUDA, "ww_ternary_gemv_plane: %s",
+                        cudaGetErrorString((cudaError_t)e32));
     cudaError_t e = launch_pdl(tern_plane_kernel, dim3(grid), dim3(kWarps * 32), smem,
                                (cudaStream_t)stream, (flags & WW_FLAG_PDL) != 0, pl, x_d, (int)comp,
                                n, m, W, acc_d);
