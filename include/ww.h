@@ -29,6 +29,13 @@
  *     plane p, row i (t = i/32, s = w/4).  Rows past n and words past W are zero codes.
  *     ww_packed_bytes_layout(): ceil(n/32) * S * 2048 bytes (2 bits per code, the same bytes
  *     as the other layouts when 32 | n and 64 | m).
+ *   WW_LAYOUT_LUT81 (device layout of the lookup path, ww_wl_gemv_lut): one byte per 4 codes
+ *     of one plane, byte = sum_k (code_k + 1) 3^k over columns 4g..4g+3 (0..80; 40 = four
+ *     zero codes) -- a bijection of the four App. H bit pairs, still 2 bits per code.  Rows
+ *     are T = ceil(m/512) steps of 512 bytes: byte 16*((i*T + t)*32 + l) + 4*p + k holds
+ *     plane p, row i, columns 512t + 128k + 4l .. +3 (padding columns are zero codes).
+ *     Converted on the host from / to WW_LAYOUT_PLANAR (ww_lut81_from_planar / _to_planar);
+ *     ww_lut81_packed_bytes(): n * T * 512.
  *
  * Scales (R2): WW_SCALES_PER_ROW = n x 4 fp32 [sUr, sUi, sWr, sWi] row-major;
  *   WW_SCALES_PER_TENSOR = 4 fp32 shared by all rows.
@@ -65,7 +72,7 @@ typedef enum {
     WW_ERR_CUDA = 8                /* a CUDA runtime call failed; see ww_last_error() */
 } ww_status;
 
-typedef enum { WW_LAYOUT_PLANAR = 0, WW_LAYOUT_COL4 = 1, WW_LAYOUT_TILE32 = 2 } ww_layout;
+typedef enum { WW_LAYOUT_PLANAR = 0, WW_LAYOUT_COL4 = 1, WW_LAYOUT_TILE32 = 2, WW_LAYOUT_LUT81 = 3 } ww_layout;
 typedef enum { WW_CONV_EQ1 = 0, WW_CONV_ALG1 = 1 } ww_convention;
 typedef enum { WW_SCALES_PER_TENSOR = 0, WW_SCALES_PER_ROW = 1 } ww_scale_mode;
 
@@ -328,6 +335,30 @@ ww_status ww_wl_gemv_batched_tc(const ww_layer* L, const void* packed_d, const f
 size_t ww_tcv_workspace_bytes(int64_t n, int64_t m, int32_t B);
 ww_status ww_wl_gemv_tc(const ww_layer* L, const void* packed_d, const float* scales_d, const float* X_d,
                         int64_t ldx, float* Y_d, int64_t ldy, int32_t B, void* workspace_d, void* stream);
+
+/* WL-GEMV by ternary subset-sum lookup (B = 1; DESIGN.md §6 "wl_lut_kernel").  Eq. 1
+ * (Eqs. 6-7) with every group of 4 codes of a plane taken as one
+ * table entry: per launch each CTA builds, with adds and subtracts only (a code
+ * selects +x, -x or nothing), the 81 sums sum_k c_k x_k, c in {-1,0,+1}^4, of each group of
+ * 4 columns of x in shared memory; a weight byte (WW_LAYOUT_LUT81) indexes it.  The scales
+ * are applied once per row after accumulation, EQ1 / ALG1 signs as ww_wl_gemv.
+ * Columns are split over the CTAs of a thread-block cluster (1024 columns each) whose
+ * per-row totals are summed in rank order through distributed shared memory: results are
+ * deterministic and independent of the row shard.  Rounding order differs from ww_wl_gemv
+ * (groups of 4 are summed first), same error bound.
+ * packed_d: ww_lut81_packed_bytes(n, m) bytes, 16-B aligned; x_d: m complex64, y_d: n
+ * complex64 (8-B aligned, must not overlap); scales as ww_wl_gemv.  WW_FLAG_PDL: the first
+ * weight loads are issued before griddepcontrol.wait, x / scales / y touched after it.
+ * Errors: WW_ERR_UNSUPPORTED (layout; m > 8192: cluster of more than 8 CTAs; more than 1536
+ * rows per cluster), argument / alignment errors before any launch.  One launch on `stream`.
+ * ww_lut81_from_planar / ww_lut81_to_planar: host conversion from / to the App. H planes
+ * (WW_LAYOUT_PLANAR); WW_ERR_INVALID_ENCODING on a (1,1) slot, a byte > 80 or a nonzero
+ * padding code (nothing defined is written past that point). */
+size_t ww_lut81_packed_bytes(int64_t n, int64_t m);
+ww_status ww_lut81_from_planar(int64_t n, int64_t m, const void* planar, void* out);
+ww_status ww_lut81_to_planar(int64_t n, int64_t m, const void* lut, void* planar_out);
+ww_status ww_wl_gemv_lut(const ww_layer* L, const void* packed_d, const float* scales_d,
+                         const float* x_d, float* y_d, void* stream);
 
 /* Keep [ptr, ptr + bytes) persisting in L2 for kernels launched on `stream` (and kernel nodes
  * captured from it): access-policy window, hit ratio 1, streaming misses; reserves up to

@@ -27,7 +27,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 OK = 0
 ERR_INVALID_ARGUMENT, ERR_DIMENSION_MISMATCH, ERR_INVALID_CODE, ERR_INVALID_ENCODING = 1, 2, 3, 4
 ERR_NONFINITE_SCALE, ERR_MISALIGNED, ERR_UNSUPPORTED, ERR_CUDA = 5, 6, 7, 8
-LAYOUT_PLANAR, LAYOUT_COL4, LAYOUT_TILE32 = 0, 1, 2
+LAYOUT_PLANAR, LAYOUT_COL4, LAYOUT_TILE32, LAYOUT_LUT81 = 0, 1, 2, 3
 CONV_EQ1, CONV_ALG1 = 0, 1
 SCALES_PER_TENSOR, SCALES_PER_ROW = 0, 1
 FLAG_PDL = 1
@@ -45,7 +45,8 @@ EXPORTS = ("ww_packed_bytes", "ww_pack_ternary", "ww_unpack_ternary", "ww_repack
            "ww_ternary_gemv_plane", "ww_wl_combine", "ww_wl_gemv_fused", "ww_program_workspace_bytes",
            "ww_program_sync_bytes", "ww_program_init", "ww_program_run", "ww_stream_keep_in_l2",
            "ww_tc_workspace_bytes", "ww_wl_gemv_batched_tc", "ww_packed_bytes_layout",
-           "ww_pack_ternary_device_layout", "ww_tcv_workspace_bytes", "ww_wl_gemv_tc")
+           "ww_pack_ternary_device_layout", "ww_tcv_workspace_bytes", "ww_wl_gemv_tc",
+           "ww_lut81_packed_bytes", "ww_lut81_from_planar", "ww_lut81_to_planar", "ww_wl_gemv_lut")
 
 
 class WWError(RuntimeError):
@@ -148,6 +149,14 @@ _lib.ww_tcv_workspace_bytes.argtypes = [_i64, _i64, _i32]
 _lib.ww_wl_gemv_tc.restype = _i32
 _lib.ww_wl_gemv_tc.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _vp]
 _lib.ww_stream_keep_in_l2.restype = _i32
+_lib.ww_lut81_packed_bytes.restype = ctypes.c_size_t
+_lib.ww_lut81_packed_bytes.argtypes = [_i64, _i64]
+_lib.ww_lut81_from_planar.restype = _i32
+_lib.ww_lut81_from_planar.argtypes = [_i64, _i64, _vp, _vp]
+_lib.ww_lut81_to_planar.restype = _i32
+_lib.ww_lut81_to_planar.argtypes = [_i64, _i64, _vp, _vp]
+_lib.ww_wl_gemv_lut.restype = _i32
+_lib.ww_wl_gemv_lut.argtypes = [ctypes.POINTER(_Layer), _vp, _vp, _vp, _vp, _vp]
 _lib.ww_stream_keep_in_l2.argtypes = [_vp, _vp, ctypes.c_size_t]
 _lib.ww_status_string.restype = ctypes.c_char_p
 _lib.ww_status_string.argtypes = [_i32]
@@ -556,3 +565,56 @@ def wl_gemv_tc(layer: Layer, packed, scales, X, Y=None, workspace=None, stream=N
                               X2.stride(0), Y2.data_ptr(), Y2.stride(0), B, workspace.data_ptr(),
                               _stream_ptr(stream)))
     return Y
+
+
+# --------------------------------------------------------------------------- lookup path (LUT81)
+def lut81_packed_bytes(n: int, m: int) -> int:
+    return int(_lib.ww_lut81_packed_bytes(n, m))
+
+
+def lut81_from_planar(planar: np.ndarray, n: int, m: int) -> np.ndarray:
+    """App. H planar words -> WW_LAYOUT_LUT81 bytes (host, ww_lut81_from_planar)."""
+    planar = np.ascontiguousarray(planar, dtype=np.uint32)
+    if planar.size * 4 != packed_bytes(n, m, LAYOUT_PLANAR):
+        raise ValueError("planar buffer has the wrong size")
+    out = np.empty(lut81_packed_bytes(n, m), np.uint8)
+    _check(_lib.ww_lut81_from_planar(n, m, planar.ctypes.data, out.ctypes.data))
+    return out
+
+
+def lut81_to_planar(lut: np.ndarray, n: int, m: int) -> np.ndarray:
+    """WW_LAYOUT_LUT81 bytes -> App. H planar words (host, ww_lut81_to_planar)."""
+    lut = np.ascontiguousarray(lut, dtype=np.uint8)
+    if lut.size != lut81_packed_bytes(n, m):
+        raise ValueError("LUT81 buffer has the wrong size")
+    out = np.empty(packed_bytes(n, m, LAYOUT_PLANAR) // 4, np.uint32)
+    _check(_lib.ww_lut81_to_planar(n, m, lut.ctypes.data, out.ctypes.data))
+    return out
+
+
+def pack_lut81(planes: np.ndarray) -> np.ndarray:
+    """(4, n, m) int8 planes -> WW_LAYOUT_LUT81 bytes (host: App. H words, then the index bytes)."""
+    _, n, m = planes.shape
+    return lut81_from_planar(pack_ternary(planes, LAYOUT_PLANAR), n, m)
+
+
+def wl_gemv_lut(layer: Layer, packed, scales, x, y=None, stream=None):
+    """y = WL-GEMV(x) by ternary subset-sum lookup (ww_wl_gemv_lut; LUT81 weights, B = 1)."""
+    import torch
+    if layer.layout != LAYOUT_LUT81:
+        raise ValueError("wl_gemv_lut needs layout LAYOUT_LUT81")
+    if y is None:
+        y = torch.empty(layer.n, dtype=torch.complex64, device=x.device)
+    for name, t, dt in (("x", x, torch.complex64), ("y", y, torch.complex64), ("scales", scales, torch.float32)):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dt or not t.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous CUDA tensor of {dt}")
+    if x.numel() != layer.m or y.numel() != layer.n:
+        raise ValueError("x / y length does not match the layer")
+    if scales.numel() != (4 * layer.n if layer.scale_mode == SCALES_PER_ROW else 4):
+        raise ValueError("scales size does not match the layer")
+    if not packed.is_cuda or packed.numel() * packed.element_size() < lut81_packed_bytes(layer.n, layer.m):
+        raise ValueError("packed buffer too small for WW_LAYOUT_LUT81")
+    L = layer.c()
+    _check(_lib.ww_wl_gemv_lut(ctypes.byref(L), packed.data_ptr(), scales.data_ptr(), x.data_ptr(),
+                               y.data_ptr(), _stream_ptr(stream)))
+    return y
