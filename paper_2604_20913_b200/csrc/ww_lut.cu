@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 
 #include "ww_internal.h"
 
@@ -35,6 +36,8 @@ constexpr int kStepBytes = 4 * kBlockBytes;
 constexpr int kMaxStepsPerCta = 2;      // 8 blocks = 165,888 B of tables
 constexpr int kMaxRowsPerCluster = 1536;  // 48 KB of partial totals
 constexpr int kMaxCluster = 8;
+// tables start at a 64 KB boundary: with the window's first 1 KB reserved, 63 KB in front of them
+constexpr int kDynSmem = 0x10000 + kMaxStepsPerCta * kStepBytes;  // 231,424 B: any window offset >= 0
 
 struct LutParams {
     const uint4* Wp;      // [n][T][32] uint4
@@ -53,11 +56,6 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
                  : "l"(p));
     return v;
 }
-__device__ __forceinline__ float2 lds64(uint32_t a) {
-    float2 v;
-    asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-    return v;
-}
 __device__ __forceinline__ void sts64(uint32_t a, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -73,16 +71,21 @@ __device__ __forceinline__ void pair9(float2 a, float2 b, float2 (&t)[9]) {
 }
 
 // one plane word = 4 bytes = the lane's group in 4 consecutive blocks
-template <int K>
-__device__ __forceinline__ void lookup(float2& acc, uint32_t w, uint32_t base) {
-    const uint32_t off = __byte_perm(w, 0u, 0x4404 | (K << 4));  // byte K -> bits 8..15
-    acc = add2(acc, lds64(base + off + K * kBlockBytes));
+// base = table address (a multiple of 64 KB) + lane * 8: byte 1 of the address is the index
+template <int OFF>
+__device__ __forceinline__ void lookup(float2& acc, uint32_t w, uint32_t base, int k) {
+    const uint32_t a = __byte_perm(w, base, 0x7604 | (k << 4));  // byte k of w -> bits 8..15
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0,%1}, [%2+%3];" : "=f"(v.x), "=f"(v.y) : "r"(a), "n"(OFF));
+    acc = add2(acc, v);
 }
+// one plane word = 4 bytes = the lane's group in 4 consecutive blocks of step STEP of the CTA
+template <int STEP>
 __device__ __forceinline__ void plane4(float2& acc, uint32_t w, uint32_t base) {
-    lookup<0>(acc, w, base);
-    lookup<1>(acc, w, base);
-    lookup<2>(acc, w, base);
-    lookup<3>(acc, w, base);
+    lookup<STEP * kStepBytes + 0 * kBlockBytes>(acc, w, base, 0);
+    lookup<STEP * kStepBytes + 1 * kBlockBytes>(acc, w, base, 1);
+    lookup<STEP * kStepBytes + 2 * kBlockBytes>(acc, w, base, 2);
+    lookup<STEP * kStepBytes + 3 * kBlockBytes>(acc, w, base, 3);
 }
 
 // totals over the 32 lanes of the 8 values in a[4] (x = re, y = im of plane p): value v ends
@@ -123,9 +126,52 @@ __device__ __forceinline__ uint4 load_item(const uint4* wp, int64_t stride, int 
     return ldg_stream(wp + (int64_t)row * stride + s * 32);
 }
 
+// predicated 128-bit streaming load: v keeps its value when !pred
+__device__ __forceinline__ void ldg_stream_if(uint4& v, const uint4* p, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "l"(p), "r"((uint32_t)pred));
+}
+
+// slot J of the ring holds item q + J = (row (q + J) / NSTEPS, step (q + J) % NSTEPS); its
+// lookups, the refill with item q + J + kRing from `next` (when LOAD), and the row's end
+template <int NSTEPS, int J, bool LOAD>
+__device__ __forceinline__ void ring_item(const uint4* next, int64_t stride, int q, int Q, uint32_t base,
+                                          float* part, int lane, int vi, uint4 (&buf)[kRing],
+                                          float2 (&acc)[4]) {
+    const uint4 w = buf[J];
+    if (LOAD)
+        ldg_stream_if(buf[J], next + (int64_t)(J / NSTEPS) * stride + (J % NSTEPS) * 32,
+                      q + J + kRing < Q);
+    constexpr int kStep = NSTEPS == 2 ? (J & 1) : 0;
+    plane4<kStep>(acc[0], w.x, base);
+    plane4<kStep>(acc[1], w.y, base);
+    plane4<kStep>(acc[2], w.z, base);
+    plane4<kStep>(acc[3], w.w, base);
+    if (NSTEPS == 1 || (J & 1)) {  // the row's last step
+        const float r = reduce8(acc, lane);
+        if ((lane & 3) == 0) part[(q + J) / NSTEPS * 8 + vi] = r;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
+    }
+}
+
+#define WW_RING_ITEMS(LOAD, GUARD)                                                              \
+    if (!(GUARD) || q + 0 < Q) ring_item<NSTEPS, 0, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
+    if (!(GUARD) || q + 1 < Q) ring_item<NSTEPS, 1, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
+    if (!(GUARD) || q + 2 < Q) ring_item<NSTEPS, 2, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
+    if (!(GUARD) || q + 3 < Q) ring_item<NSTEPS, 3, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
+    if (!(GUARD) || q + 4 < Q) ring_item<NSTEPS, 4, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
+    if (!(GUARD) || q + 5 < Q) ring_item<NSTEPS, 5, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
+    if (!(GUARD) || q + 6 < Q) ring_item<NSTEPS, 6, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
+    if (!(GUARD) || q + 7 < Q) ring_item<NSTEPS, 7, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc);
+
 template <int NSTEPS>
 __device__ __forceinline__ void sweep_rows(const uint4* wp, int64_t stride, int nrows, uint32_t tab,
                                            float* part, int lane, uint4 (&buf)[kRing]) {
+    static_assert(kRing == 8, "WW_RING_ITEMS");
     const int Q = nrows * NSTEPS;
     float2 acc[4];
 #pragma unroll
@@ -133,27 +179,16 @@ __device__ __forceinline__ void sweep_rows(const uint4* wp, int64_t stride, int 
     const uint32_t base = tab + lane * 8;
     // value index held by this lane after reduce8
     const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-    for (int q = 0; q < Q; q += kRing) {
-#pragma unroll
-        for (int j = 0; j < kRing; ++j) {
-            if (q + j < Q) {
-                const uint4 w = buf[j];
-                if (q + j + kRing < Q) buf[j] = load_item(wp, stride, q + j + kRing, NSTEPS);
-                const uint32_t b = base + ((NSTEPS == 2 && (j & 1)) ? kStepBytes : 0);
-                plane4(acc[0], w.x, b);
-                plane4(acc[1], w.y, b);
-                plane4(acc[2], w.z, b);
-                plane4(acc[3], w.w, b);
-                if (NSTEPS == 1 || (j & 1)) {  // the row's last step
-                    const float r = reduce8(acc, lane);
-                    if ((lane & 3) == 0) part[(q + j) / NSTEPS * 8 + vi] = r;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
-                }
-            }
-        }
+    const int64_t adv = (int64_t)(kRing / NSTEPS) * stride;  // one ring of items further
+    const uint4* wq = wp;
+    int q = 0;
+    for (; q + kRing <= Q; q += kRing) {  // full rings: no guards around the lookups
+        wq += adv;
+        WW_RING_ITEMS(true, false)
     }
+    WW_RING_ITEMS(false, true)  // the tail: items already in the ring
 }
+#undef WW_RING_ITEMS
 
 __global__ void __launch_bounds__(kThreads, 1) wl_lut_kernel(const LutParams p) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -178,8 +213,14 @@ __global__ void __launch_bounds__(kThreads, 1) wl_lut_kernel(const LutParams p) 
     const int nsteps = max(0, min(Tc, p.T - t0));
 
     float* part = reinterpret_cast<float*>(smem);  // [NR][8] partial totals of this CTA
-    const uint32_t tab =
-        (uint32_t)__cvta_generic_to_shared(smem) + kMaxRowsPerCluster * 32;  // tables
+    // tables at the first 64 KB boundary of the shared window past the partial totals (bits
+    // 8..15 of a lookup address are then the index alone); in a cluster the CTA's window
+    // does not start near 0, only its offset within 64 KB matters
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t tab = (sbase + kMaxRowsPerCluster * 32 + 0xFFFFu) & ~0xFFFFu;
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (tab + kMaxStepsPerCta * kStepBytes > sbase + dyn) __trap();
 
     // the weights never depend on the previous kernel: the first loads go out before the wait
     const uint4* wp = p.Wp + ((r0 + w0) * p.T + t0) * 32 + lane;
@@ -254,6 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1) wl_lut_kernel(const LutParams p) 
 }
 
 inline int lut_steps(int64_t m) { return (int)((m + 511) / 512); }
+
+std::mutex g_lut_mu;
+int g_resident[64][kMaxCluster + 1] = {};  // resident clusters per (device, cluster size); 0 = not queried
 
 }  // namespace
 
@@ -346,16 +390,42 @@ extern "C" ww_status ww_wl_gemv_lut(const ww_layer* L, const void* packed_d, con
         return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv_lut: m=%lld needs a cluster of %d CTAs (max %d)",
                         (long long)L->m, S, kMaxCluster);
     const int sms = ww::device_sms();
-    const int C = (int)std::max<int64_t>(1, std::min<int64_t>(sms / S, L->n));
+    const size_t smem = kDynSmem;
+    const int e = ww::prepare_kernel(reinterpret_cast<const void*>(wl_lut_kernel), kDynSmem);
+    if (e)
+        return ww::fail(WW_ERR_CUDA, "ww_wl_gemv_lut: %s", cudaGetErrorString((cudaError_t)e));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sms / S * S);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // one wave: no more clusters than can be resident at once (GPC boundaries)
+    int resident;
+    {
+        const int dev = ww::current_device();
+        std::lock_guard<std::mutex> lk(g_lut_mu);
+        int& slot = g_resident[dev >= 0 && dev < 64 ? dev : 0][S];
+        if (slot == 0) {
+            int r = 0;
+            if (cudaOccupancyMaxActiveClusters(&r, wl_lut_kernel, &cfg) != cudaSuccess || r < 1) {
+                cudaGetLastError();
+                r = std::max(1, sms / S);
+            }
+            slot = r;
+        }
+        resident = slot;
+    }
+    const int C = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(sms / S, resident), L->n));
     if ((L->n + C - 1) / C > kMaxRowsPerCluster)
         return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv_lut: n=%lld exceeds %d rows per cluster",
                         (long long)L->n, kMaxRowsPerCluster);
-    const int Tc = (T + S - 1) / S;
-    const size_t smem = (size_t)kMaxRowsPerCluster * 32 + (size_t)Tc * kStepBytes;
-    const int e = ww::prepare_kernel(reinterpret_cast<const void*>(wl_lut_kernel),
-                                      kMaxRowsPerCluster * 32 + kMaxStepsPerCta * kStepBytes);
-    if (e)
-        return ww::fail(WW_ERR_CUDA, "ww_wl_gemv_lut: %s", cudaGetErrorString((cudaError_t)e));
     LutParams p;
     p.Wp = static_cast<const uint4*>(packed_d);
     p.scales = scales_d;
@@ -368,19 +438,9 @@ extern "C" ww_status ww_wl_gemv_lut(const ww_layer* L, const void* packed_d, con
     p.per_row = L->scale_mode == WW_SCALES_PER_ROW;
     p.conv = L->conv;
     p.pdl = (L->flags & WW_FLAG_PDL) != 0;
-    cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C * S);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = (cudaStream_t)stream;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = S;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
-    cfg.attrs = attr;
     cfg.numAttrs = 2;
     const cudaError_t le = cudaLaunchKernelEx(&cfg, wl_lut_kernel, p);
     if (le != cudaSuccess)
