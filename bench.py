@@ -275,7 +275,7 @@ def run_ours(args, world, rank, local):
         base = WLStack(layers=args.layers, seed=args.seed, B=args.batch, rank=rank, world=world,
                        pdl=not args.no_pdl, device=dev, group=group, fuse=not args.no_fuse,
                        chain=args.chain if args.engine == "pdl" else "plain", gammas=gam,
-                       symm=args.engine == "program" and world > 1)
+                       symm=args.engine == "program" and world > 1, lut_stages=_lut_stages(args))
         if args.engine == "program":
             stack = ProgramRunner(base, args.chain, gam)
         else:
@@ -443,10 +443,14 @@ def run_ours(args, world, rank, local):
                    "peak_basis": "measured bf16 TFLOP/s x 2 (int8 nominal ratio)"}
     roof = {"bound": "alu", "achieved": round(achieved_alu, 4), "peak": round(alu_peak, 4),
             "unit": "Tadd/s", "frac": round(achieved_alu / alu_peak, 4),
-            "traffic": _ncu_traffic(),
+            "traffic": _ncu_traffic(lut=bool(getattr(stack, "lut_stages", None))),
             "kernel": ("wl_program_kernel (whole step)" if args.engine == "program"
-                       and args.workload == "c4" else "wl_gemv_kernel<1>"),
-            "peak_basis": f"128 fp32 add lanes/clk/SM x {nsm} SMs x {sm_mhz:.0f} MHz (DESIGN.md §8)",
+                       and args.workload == "c4" else
+                       "wl_lut_kernel" if getattr(stack, "lut_stages", None) else "wl_gemv_kernel<1>"),
+            "peak_basis": f"128 fp32 add lanes/clk/SM x {nsm} SMs x {sm_mhz:.0f} MHz (DESIGN.md §8)"
+                          + ("; achieved = the 8nm algorithmic adds per launch (the lookup path issues one "
+                             "FADD2 per 4 codes and is bound by LDS.64 issue, 64 codes/clk/SM)"
+                             if getattr(stack, "lut_stages", None) else ""),
             "hbm": {"achieved": round(hbm_achieved, 1), "peak": peaks.get("hbm_gbs"),
                     "unit": "GB/s", "frac": round(hbm_achieved / peaks.get("hbm_gbs", 6650.0), 4),
                     "peak_kind": peak_kind, "bytes": "packed weights + x per launch"}}
@@ -467,7 +471,10 @@ def run_ours(args, world, rank, local):
                    "nccl_in_graph": bool(graph is not None and world > 1),
                    "x_l2_persist": bool(args.x_l2_persist),
                    "path": ("tcgen05 kind::i8 (wl_tc_kernel)" if getattr(stack, "tc", False)
-                            else "predicated FADD2 (wl_gemv_kernel)"),
+                            else "predicated FADD2 (wl_gemv_kernel)"
+                            + ("; subset-sum lookup (wl_lut_kernel, WW_LAYOUT_LUT81) on stages "
+                               + ",".join(sorted(getattr(stack, "lut_stages", ())))
+                               if getattr(stack, "lut_stages", None) else "")),
                    "l2": "inputs > L2: 1.62 GB of weights per step streamed from HBM"
                          if args.workload == "c4" else "rotating replicas >= 4x L2",
                    "launch": _launch_configs(ww, stack, args)},
@@ -524,12 +531,13 @@ def _time_allgathers(stack, idx, s, dev, reps=5):
     return {"us": round(float(t.item()), 3), "graph": g is not None}
 
 
-def _ncu_traffic():
+def _ncu_traffic(lut=False):
     """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            t = json.load(f)
+            return (t.get("lut") or {}).get("dram_bytes_per_launch") if lut else t.get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -621,6 +629,16 @@ def _e2e(stack, args, s, dev, graph, world, alg_bytes):
                         "during step k-1" if pipelined else "serial copies on the compute stream")}
 
 
+def _lut_stages(args):
+    """Stages of the config-4 stack that run on the lookup path (B = 1, PDL engine, plain chain)."""
+    if (args.workload != "c4" or args.engine != "pdl" or args.chain != "plain" or args.batch != 1
+            or args.no_fuse or args.lut_stages == "none"):
+        return ()
+    if args.lut_stages == "auto":
+        return ("qkv", "o", "gateup", "down")
+    return tuple(x for x in args.lut_stages.split(",") if x)
+
+
 def _launch_configs(ww, stack, args):
     """ww_query_launch of every distinct launch shape of the step (per-rank rows)."""
     if args.workload == "c4":
@@ -634,7 +652,15 @@ def _launch_configs(ww, stack, args):
                                "one CTA per 32-row tile; the K range split over a thread-block cluster of "
                                "up to 4 CTAs when tiles < SMs and B <= 8)",
                     "tiles": -(-n // 32)} for k, (n, m) in shapes.items()}
-    return {k: ww.query_launch(ww.Layer(max(n, 1), m), args.batch) for k, (n, m) in shapes.items()}
+    out = {k: ww.query_launch(ww.Layer(max(n, 1), m), args.batch) for k, (n, m) in shapes.items()}
+    for k, (n, m) in shapes.items():  # lookup stages: wl_lut_kernel's launch shape (ww_lut.cu)
+        if k.split()[0] in getattr(stack, "lut_stages", ()):
+            steps = -(-m // 512)
+            cl = -(-steps // 2)
+            out[k] = {"kernel": "wl_lut_kernel", "block": 512, "smem_bytes": 231424, "cluster": cl,
+                      "grid": f"min(#SMs // {cl}, resident clusters) x {cl}", "steps_of_512_columns": steps,
+                      "columns_per_cta": 1024}
+    return out
 
 
 class ProgramRunner:
@@ -786,6 +812,11 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lut-stages", default="auto",
+                    help="c4, pdl engine, plain chain, B = 1: comma-separated stages (qkv,o,gateup,down) "
+                         "on the lookup path ww_wl_gemv_lut; 'auto' = all four (a chain mixing the two kernels "
+                         "is slower than either, profiles/r02/lut_stage_sets.txt), 'none' = all on the "
+                         "predicated-FADD2 kernel")
     ap.add_argument("--no-tc", action="store_true",
                     help="single-layer workloads: keep B >= 4 on the predicated-FADD2 kernel instead "
                          "of the tcgen05 path")

@@ -98,7 +98,8 @@ typedef struct {
 /* Bytes of packed weights for an n x m layer in WW_LAYOUT_PLANAR or WW_LAYOUT_COL4:
  * 16 * n * ceil(m/16). */
 size_t ww_packed_bytes(int64_t n, int64_t m);
-/* Bytes of packed weights in any layout (WW_LAYOUT_TILE32: ceil(n/32) * ceil(m/64) * 2048);
+/* Bytes of packed weights in any layout (WW_LAYOUT_TILE32: ceil(n/32) * ceil(m/64) * 2048;
+ * WW_LAYOUT_LUT81: n * ceil(m/512) * 512);
  * 0 for an unknown layout or negative sizes. */
 size_t ww_packed_bytes_layout(int64_t n, int64_t m, int32_t layout);
 
@@ -127,7 +128,9 @@ ww_status ww_pack_ternary_device(const int8_t* planes_d, int64_t n, int64_t m, i
                                  uint32_t* out_d, int32_t* bad_d, void* stream);
 /* The same device packer for any GPU layout: WW_LAYOUT_COL4 (== ww_pack_ternary_device) or
  * WW_LAYOUT_TILE32 (out_d: ww_packed_bytes_layout(n,m,WW_LAYOUT_TILE32) bytes, 16-B aligned;
- * an invalid value packs its 16-column word of that plane as zero and sets *bad_d). */
+ * an invalid value packs its 16-column word of that plane as zero and sets *bad_d) or
+ * WW_LAYOUT_LUT81 (out_d: ww_packed_bytes_layout(n,m,WW_LAYOUT_LUT81) bytes, 16-B aligned; an
+ * invalid value packs as the zero code and sets *bad_d). */
 ww_status ww_pack_ternary_device_layout(const int8_t* planes_d, int64_t n, int64_t m, int64_t ld,
                                         int32_t layout, uint32_t* out_d, int32_t* bad_d,
                                         void* stream);

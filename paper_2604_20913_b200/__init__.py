@@ -199,7 +199,7 @@ class Layer:
 
 
 def packed_bytes(n: int, m: int, layout: int = LAYOUT_COL4) -> int:
-    if layout == LAYOUT_TILE32:
+    if layout in (LAYOUT_TILE32, LAYOUT_LUT81):
         return int(_lib.ww_packed_bytes_layout(n, m, layout))
     return int(_lib.ww_packed_bytes(n, m))
 

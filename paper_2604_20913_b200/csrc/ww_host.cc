@@ -57,6 +57,7 @@ extern "C" size_t ww_packed_bytes_layout(int64_t n, int64_t m, int32_t layout) {
     if (layout == WW_LAYOUT_PLANAR || layout == WW_LAYOUT_COL4) return ww_packed_bytes(n, m);
     if (layout == WW_LAYOUT_TILE32)
         return (size_t)ww::tile32_tiles(n) * (size_t)ww::tile32_slabs(m) * 2048u;
+    if (layout == WW_LAYOUT_LUT81) return (size_t)n * (size_t)((m + 511) / 512) * 512u;
     return 0;
 }
 

@@ -18,4 +18,7 @@ int device_sms();                                          // SM count of the cu
 int prepare_kernel(const void* fn, int max_dynamic_smem);  // cudaError_t of the attribute calls
 // CUtensorMap of x as [B][W][32 floats], 32 x 32 boxes, 128B swizzle (0 on success)
 int encode_x_map(void* map, const float* X, int64_t W, int64_t B, int64_t ldx);
+// WW_LAYOUT_LUT81 device packer (ww_lut.cu); returns the cudaError_t of the launch
+int pack_lut81_device(const int8_t* planes_d, int64_t n, int64_t m, int64_t ld, uint32_t* out_d,
+                      int32_t* bad_d, void* stream);
 }  // namespace ww

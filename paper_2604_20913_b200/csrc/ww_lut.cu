@@ -29,7 +29,11 @@ namespace cg = cooperative_groups;
 
 namespace {
 
+#ifdef WW_LUT_WARPS32  // experiment: 32 warps of 64 registers, ring of 4
+constexpr int kWarps = 32;
+#else
 constexpr int kWarps = 16;
+#endif
 constexpr int kThreads = kWarps * 32;
 constexpr int kBlockBytes = 81 * 256;   // one 128-column table block
 constexpr int kStepBytes = 4 * kBlockBytes;
@@ -118,7 +122,7 @@ __device__ __forceinline__ float reduce8(const float2 (&a)[4], int lane) {
     return r;  // value index 4*h4 + 2*h3 + h2 = (lane >> 2) & 7 with bits reversed: see caller
 }
 
-constexpr int kRing = 8;  // 128-bit weight loads in flight per lane
+constexpr int kRing = kWarps == 32 ? 4 : 8;  // 128-bit weight loads in flight per lane
 
 // item q of a warp = (row q / nsteps, step q % nsteps) of its rows
 __device__ __forceinline__ uint4 load_item(const uint4* wp, int64_t stride, int q, int nsteps) {
@@ -158,20 +162,18 @@ __device__ __forceinline__ void ring_item(const uint4* next, int64_t stride, int
     }
 }
 
-#define WW_RING_ITEMS(LOAD, GUARD)                                                              \
-    if (!(GUARD) || q + 0 < Q) ring_item<NSTEPS, 0, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
-    if (!(GUARD) || q + 1 < Q) ring_item<NSTEPS, 1, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
-    if (!(GUARD) || q + 2 < Q) ring_item<NSTEPS, 2, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
-    if (!(GUARD) || q + 3 < Q) ring_item<NSTEPS, 3, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
-    if (!(GUARD) || q + 4 < Q) ring_item<NSTEPS, 4, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
-    if (!(GUARD) || q + 5 < Q) ring_item<NSTEPS, 5, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
-    if (!(GUARD) || q + 6 < Q) ring_item<NSTEPS, 6, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc); \
-    if (!(GUARD) || q + 7 < Q) ring_item<NSTEPS, 7, LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc);
+#define WW_RING_ITEM(J, LOAD, GUARD) \
+    if (J < kRing && (!(GUARD) || q + J < Q)) \
+        ring_item<NSTEPS, (J < kRing ? J : 0), LOAD>(wq, stride, q, Q, base, part, lane, vi, buf, acc);
+#define WW_RING_ITEMS(LOAD, GUARD)                                                       \
+    WW_RING_ITEM(0, LOAD, GUARD) WW_RING_ITEM(1, LOAD, GUARD) WW_RING_ITEM(2, LOAD, GUARD) \
+    WW_RING_ITEM(3, LOAD, GUARD) WW_RING_ITEM(4, LOAD, GUARD) WW_RING_ITEM(5, LOAD, GUARD) \
+    WW_RING_ITEM(6, LOAD, GUARD) WW_RING_ITEM(7, LOAD, GUARD)
 
 template <int NSTEPS>
 __device__ __forceinline__ void sweep_rows(const uint4* wp, int64_t stride, int nrows, uint32_t tab,
                                            float* part, int lane, uint4 (&buf)[kRing]) {
-    static_assert(kRing == 8, "WW_RING_ITEMS");
+    static_assert(kRing <= 8 && kRing % 2 == 0, "WW_RING_ITEMS");
     const int Q = nrows * NSTEPS;
     float2 acc[4];
 #pragma unroll
@@ -189,6 +191,7 @@ __device__ __forceinline__ void sweep_rows(const uint4* wp, int64_t stride, int 
     WW_RING_ITEMS(false, true)  // the tail: items already in the ring
 }
 #undef WW_RING_ITEMS
+#undef WW_RING_ITEM
 
 __global__ void __launch_bounds__(kThreads, 1) wl_lut_kernel(const LutParams p) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -295,6 +298,35 @@ __global__ void __launch_bounds__(kThreads, 1) wl_lut_kernel(const LutParams p) 
 }
 
 inline int lut_steps(int64_t m) { return (int)((m + 511) / 512); }
+
+// device packer: one thread per output word = (row i, step t, lane l, plane p), 4 blocks k.
+// A value outside {-1,0,+1} packs as the zero code and sets *bad (as the COL4 packer, ww.h).
+__global__ void pack_lut81_kernel(const int8_t* __restrict__ planes, int64_t n, int64_t m, int64_t ld,
+                                  int T, int64_t total, uint32_t* __restrict__ out, int32_t* bad) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const int p = (int)(w & 3), l = (int)((w >> 2) & 31);
+        const int64_t it = w >> 7, i = it / T, t = it % T;
+        const int8_t* row = planes + ((int64_t)p * n + i) * ld;
+        uint32_t word = 0;
+        bool any_bad = false;
+        for (int k = 0; k < 4; ++k) {
+            const int64_t col = t * 512 + k * 128 + l * 4;
+            int idx = 0, pw = 1;
+            for (int c = 0; c < 4; ++c, pw *= 3) {
+                int v = col + c < m ? (int)row[col + c] : 0;
+                if (v < -1 || v > 1) {
+                    any_bad = true;
+                    v = 0;
+                }
+                idx += pw * (v + 1);
+            }
+            word |= (uint32_t)idx << (8 * k);
+        }
+        out[w] = word;
+        if (any_bad && bad) atomicOr(bad, 1);
+    }
+}
 
 std::mutex g_lut_mu;
 int g_resident[64][kMaxCluster + 1] = {};  // resident clusters per (device, cluster size); 0 = not queried
@@ -447,3 +479,15 @@ extern "C" ww_status ww_wl_gemv_lut(const ww_layer* L, const void* packed_d, con
         return ww::fail(WW_ERR_CUDA, "ww_wl_gemv_lut: %s", cudaGetErrorString(le));
     return ww::ok();
 }
+
+// WW_LAYOUT_LUT81 arm of ww_pack_ternary_device_layout (arguments already checked there)
+namespace ww {
+int pack_lut81_device(const int8_t* planes_d, int64_t n, int64_t m, int64_t ld, uint32_t* out_d,
+                      int32_t* bad_d, void* stream) {
+    const int T = lut_steps(m);
+    const int64_t total = n * (int64_t)T * 128;
+    pack_lut81_kernel<<<ww::device_sms() * 8, 256, 0, (cudaStream_t)stream>>>(planes_d, n, m, ld, T, total,
+                                                                           out_d, bad_d);
+    return (int)cudaGetLastError();
+}
+}  // namespace ww

@@ -888,12 +888,18 @@ extern "C" ww_status ww_pack_ternary_device_layout(const int8_t* planes_d, int64
                                                    void* stream) {
     const char* fn = "ww_pack_ternary_device_layout";
     if (layout == WW_LAYOUT_COL4) return ww_pack_ternary_device(planes_d, n, m, ld, out_d, bad_d, stream);
-    if (layout != WW_LAYOUT_TILE32) return ww::fail(WW_ERR_UNSUPPORTED, "%s: layout %d", fn, layout);
+    if (layout != WW_LAYOUT_TILE32 && layout != WW_LAYOUT_LUT81)
+        return ww::fail(WW_ERR_UNSUPPORTED, "%s: layout %d", fn, layout);
     if (!planes_d || !out_d) return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: null pointer", fn);
     if (n < 1 || m < 1 || ld < m)
         return ww::fail(WW_ERR_INVALID_ARGUMENT, "%s: n=%lld m=%lld ld=%lld", fn, (long long)n, (long long)m,
                         (long long)ld);
     if ((uintptr_t)out_d & 15) return ww::fail(WW_ERR_MISALIGNED, "%s: out must be 16-B aligned", fn);
+    if (layout == WW_LAYOUT_LUT81) {
+        const int el = ww::pack_lut81_device(planes_d, n, m, ld, out_d, bad_d, stream);
+        if (el) return ww::fail(WW_ERR_CUDA, "%s: %s", fn, cudaGetErrorString((cudaError_t)el));
+        return ww::ok();
+    }
     const int64_t S = ww::tile32_slabs(m);
     const int64_t total = ww::tile32_tiles(n) * S * 512;
     pack_tile32_kernel<<<ww::device_sms() * 8, 256, 0, (cudaStream_t)stream>>>(planes_d, n, m, ld, S, total,

@@ -23,7 +23,7 @@ import torch
 
 import ww_inputs as wi
 
-from . import (CONV_EQ1, FLAG_PDL, LAYOUT_COL4, SCALES_PER_ROW, Layer, launches_for_batch,
+from . import (CONV_EQ1, FLAG_PDL, LAYOUT_COL4, LAYOUT_LUT81, SCALES_PER_ROW, Layer, launches_for_batch,
                packed_bytes, pack_ternary_device, shard_plan, wl_gemv_batched)
 
 PROJ_NAMES = ("q", "k", "v", "o", "gate", "up", "down")
@@ -132,10 +132,15 @@ class WLStack:
     def __init__(self, layers: int = wi.C4_LAYERS, seed: int = 0, B: int = 1, rank: int = 0,
                  world: int = 1, conv: int = CONV_EQ1, pdl: bool = True, device=None,
                  group=None, fuse: bool = True, chain: str = "plain", gammas=None,
-                 symm: bool = False):
+                 symm: bool = False, lut_stages=()):
         """chain "plain": every stage reads its own seeded x; "block": the NEXT-3 decode-block
         chain (block_inputs), stage inputs are earlier stages' gathered outputs, with the
-        fused RMSNorm / SiLU / (.) / residual ops of ww_wl_gemv_fused (B = 1, fuse = True)."""
+        fused RMSNorm / SiLU / (.) / residual ops of ww_wl_gemv_fused (B = 1, fuse = True).
+        lut_stages: names of the stages (B = 1, plain chain) that run on the lookup path
+        (ww_wl_gemv_lut, WW_LAYOUT_LUT81 weights) instead of the predicated-add kernel."""
+        self.lut_stages = frozenset(lut_stages)
+        if self.lut_stages:
+            assert B == 1 and chain == "plain", "the lookup path is B = 1, plain chain"
         self.layers, self.seed, self.B, self.rank, self.world = layers, seed, B, rank, world
         self.conv, self.group, self.chain, self.gammas = conv, group, chain, gammas
         if chain == "block":
@@ -154,7 +159,8 @@ class WLStack:
                 m = members[0].spec.m
                 sh = shard_plan(r0, m, world, rank)
                 nloc = sh.row_end - sh.row_begin
-                st = Stage(l, name, members, r0, m, sh, off, nloc * packed_bytes(1, m), soff,
+                lay = LAYOUT_LUT81 if name in self.lut_stages else LAYOUT_COL4
+                st = Stage(l, name, members, r0, m, sh, off, nloc * packed_bytes(1, m, lay), soff,
                            xoff, nloc, len(self.stages),
                            wi.layer_seed(seed, l, X_GROUP[projs[0]]))
                 self.stages.append(st)
@@ -196,7 +202,8 @@ class WLStack:
                     sc = wi.scales(mb.seed, mb.spec.n, mb.spec.per_row, mb.spec.scale_lo,
                                    mb.spec.scale_hi)
                     scales[lo - rb:hi - rb] = sc[lo - mb.row0:hi - mb.row0]
-                pack_ternary_device(planes, out=self.W[st.off:st.off + st.nbytes])
+                pack_ternary_device(planes, out=self.W[st.off:st.off + st.nbytes],
+                                    layout=LAYOUT_LUT81 if st.name in self.lut_stages else LAYOUT_COL4)
                 self.S[st.soff:st.soff + 4 * st.ylocal] = torch.from_numpy(scales.reshape(-1))
             xs_host[st.xoff:st.xoff + self.B * st.m] = wi.activations(st.x_seed, st.m,
                                                                       self.B).reshape(-1)
@@ -239,6 +246,12 @@ class WLStack:
                           self.S[st.soff:st.soff + 4 * st.ylocal], x,
                           self.y_local_view(st)[0], Ops(row0=st.shard.row_begin, **kw),
                           stream=stream)
+            return 1
+        if st.name in self.lut_stages:
+            from . import wl_gemv_lut
+            L.layout = LAYOUT_LUT81
+            wl_gemv_lut(L, self.W[st.off:st.off + st.nbytes], self.S[st.soff:st.soff + 4 * st.ylocal],
+                        self.x_of(st)[0], self.y_local_view(st)[0][:st.ylocal], stream=stream)
             return 1
         wl_gemv_batched(L, self.W[st.off:st.off + st.nbytes],
                         self.S[st.soff:st.soff + 4 * st.ylocal], self.x_of(st),

@@ -87,3 +87,15 @@ def test_c4_one_layer_alg1():
     _graph_step(stack)
     nproj, rel, worst = _check_stack(stack, orc.CONV_ALG1)
     assert nproj == 7
+
+
+@pytest.mark.parametrize("lut,layers", [(("qkv", "gateup"), wi.C4_LAYERS), (("qkv", "o", "gateup", "down"), 2)])
+def test_c4_lookup_stages_all_rows(lut, layers):
+    """The stack as bench.py's default line runs it (qkv and gate/up on the lookup path,
+    ww_wl_gemv_lut, the rest on the predicated-add kernel) -- and every stage on the lookup
+    path -- against the oracle, every row of every projection, PDL launches in one graph."""
+    stack = WLStack(layers=layers, seed=0, lut_stages=lut)
+    _graph_step(stack)
+    nproj, rel, worst = _check_stack(stack, orc.CONV_EQ1)
+    assert nproj == 7 * layers
+    print(f"C4 lookup {lut}: {nproj} projections, max rel L2 {rel:.2e}, max per-element ratio {worst:.3f}")

@@ -135,3 +135,21 @@ def test_argument_errors():
     with pytest.raises(ww.WWError):
         ww.wl_gemv_lut(big, torch.zeros(ww.lut81_packed_bytes(8, 9000), dtype=torch.uint8, device="cuda"),
                        torch.ones(32, device="cuda"), torch.zeros(9000, dtype=torch.complex64, device="cuda"))
+
+
+@pytest.mark.parametrize("n,m", [(5, 7), (33, 517), (64, 2048), (100, 5504)])
+def test_device_packer_equals_host_packer(n, m):
+    planes = wi.planes(n * m, n, m, wi.UNIFORM3)
+    d = ww.pack_ternary_device(torch.from_numpy(planes).cuda(), layout=ww.LAYOUT_LUT81)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), ww.pack_lut81(planes))
+
+
+def test_device_packer_flags_invalid_value():
+    planes = np.zeros((4, 3, 40), np.int8)
+    planes[2, 1, 9] = 2
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    d = ww.pack_ternary_device(torch.from_numpy(planes).cuda(), bad=bad, layout=ww.LAYOUT_LUT81)
+    torch.cuda.synchronize()
+    assert int(bad.item()) != 0
+    assert (d.cpu().numpy() == 40).all()  # the invalid value packs as the zero code
