@@ -90,3 +90,32 @@ def test_fused_ops_multiplies_stay_outside_the_loop():
             s = [_strip(l) for l in k]
             assert sum(1 for l in s if re.search(r"\bFMUL\b", l)) > 8  # ops present
             _check_loop(1, s)
+
+
+def test_lookup_kernel_has_no_fp_multiply_before_the_epilogue():
+    """wl_lut_kernel (ww_wl_gemv_lut): the table build and the lookup sweep are adds and
+    subtracts only; every floating-point multiply sits after the last lookup (the 8 scale
+    multiplies of the row epilogue), and the sweep really is one PRMT + one
+    LDS.64 + one FADD2 per 4 codes (16 of each per 128-bit weight load)."""
+    for k in _kernels_sass(r"_ZN\S*wl_lut_kernel"):
+        sass = [_strip(l) for l in k]
+        lds = [i for i, l in enumerate(sass) if re.search(r"\bLDS\.64\b", l)]
+        assert len(lds) >= 16 * 8, "expected >= 16 lookups per ring slot"
+        mul = [i for i, l in enumerate(sass) if FP_MUL.search(l)]
+        mul += [i for i, l in enumerate(sass) if re.search(r"\bHFMA2\b", l) and "-RZ, RZ" not in l]
+        assert mul, "the epilogue's scale multiplies should be FMULs"
+        # lookup runs: LDS.64 no more than 24 instructions apart (the sweeps; ptxas places the
+        # row epilogue between the two sweep instantiations, so the check is per run)
+        runs, start = [], lds[0]
+        for a, b in zip(lds, lds[1:] + [None]):
+            if b is None or b - a > 24:
+                runs.append((start, a))
+                start = b
+        assert sum(1 for a, b in runs if sum(1 for i in lds if a <= i <= b) >= 16) >= 2
+        for a, b in runs:
+            assert not [sass[i] for i in mul if a <= i <= b], (a, b)
+            region = sass[a:b + 1]
+            assert not any(re.match(r"@!?P\d\s+FADD2\b", l) for l in region), "no predicated adds here"
+        n_prmt = sum(1 for l in sass if re.search(r"\bPRMT\b", l))
+        n_add2 = sum(1 for l in sass if re.search(r"\bFADD2\b", l))
+        assert n_add2 >= len(lds) and n_prmt >= len(lds)
