@@ -410,6 +410,10 @@ extern "C" ww_status ww_wl_gemv_lut(const ww_layer* L, const void* packed_d, con
     if (L->n < 1 || L->m < 1 || L->n > ((int64_t)1 << 30))
         return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_wl_gemv_lut: n=%lld m=%lld", (long long)L->n,
                         (long long)L->m);
+    if ((L->conv != WW_CONV_EQ1 && L->conv != WW_CONV_ALG1) ||
+        (L->scale_mode != WW_SCALES_PER_ROW && L->scale_mode != WW_SCALES_PER_TENSOR))
+        return ww::fail(WW_ERR_INVALID_ARGUMENT, "ww_wl_gemv_lut: conv=%d scale_mode=%d", (int)L->conv,
+                        (int)L->scale_mode);
     if (L->layout != WW_LAYOUT_LUT81)
         return ww::fail(WW_ERR_UNSUPPORTED, "ww_wl_gemv_lut: layout %d is not WW_LAYOUT_LUT81",
                         (int)L->layout);

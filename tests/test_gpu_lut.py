@@ -131,6 +131,8 @@ def test_argument_errors():
     case = _dev(LayerCase(8, 64, seed=1))
     with pytest.raises(ValueError):
         ww.wl_gemv_lut(ww.Layer(8, 64, ww.LAYOUT_COL4), case.packed_d, case.scales_d, case.x_d[0])
+    with pytest.raises(ww.WWError):  # unknown convention
+        ww.wl_gemv_lut(ww.Layer(8, 64, ww.LAYOUT_LUT81, conv=7), case.packed_d, case.scales_d, case.x_d[0])
     big = ww.Layer(8, 9000, ww.LAYOUT_LUT81)
     with pytest.raises(ww.WWError):
         ww.wl_gemv_lut(big, torch.zeros(ww.lut81_packed_bytes(8, 9000), dtype=torch.uint8, device="cuda"),

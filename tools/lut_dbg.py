@@ -1,3 +1,5 @@
+"""Debug helper: one ww_wl_gemv_lut launch per shape, each in its own process with
+CUDA_LAUNCH_BLOCKING=1, so a faulting shape is reported without taking the others down."""
 import os, sys, subprocess
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if len(sys.argv) > 1:
